@@ -1,0 +1,69 @@
+"""Build libkronred_b200.so in-tree (sm_100a) — nvcc for the CUDA engine,
+g++ for the host C++; the shared object travels with the repo snapshot."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OUT = PKG / "_lib"
+LIB = OUT / "libkronred_b200.so"
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+NVFLAGS = COMMON + ARCH + ["-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+CXXFLAGS = COMMON + ["-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", "-I/usr/local/cuda/include"]
+
+
+def _run(cmd: list[str]) -> str:
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{p.stdout}\n{p.stderr}")
+    return p.stdout + p.stderr
+
+
+def sources() -> list[Path]:
+    return sorted(CSRC.glob("*.cpp")) + sorted(CSRC.glob("*.cu"))
+
+
+def up_to_date() -> bool:
+    if not LIB.exists():
+        return False
+    t = LIB.stat().st_mtime
+    deps = list(CSRC.glob("*")) + list((ROOT / "include").glob("*")) + [Path(__file__)]
+    return all(d.stat().st_mtime <= t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and up_to_date():
+        return LIB
+    OUT.mkdir(exist_ok=True)
+    objs, jobs = [], []
+    for src in sources():
+        obj = OUT / (src.name + ".o")
+        objs.append(obj)
+        if src.suffix == ".cu":
+            cmd = [NVCC, *NVFLAGS, "-c", str(src), "-o", str(obj)]
+        else:
+            cmd = [CXX, *CXXFLAGS, "-c", str(src), "-o", str(obj)]
+        jobs.append(cmd)
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        logs = list(ex.map(_run, jobs))
+    (OUT / "ptxas.log").write_text("\n".join(l for l in logs if l))
+    tmp = LIB.with_suffix(".so.tmp")
+    _run([NVCC, "-shared", *ARCH, "-o", str(tmp), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    os.replace(tmp, LIB)
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,766 @@
+// C ABI (include/kronred_b200.h) and the C++ drop-in entry points
+// (include/kronred_b200.hpp): input parsing, problem construction and result
+// marshalling around the device Engine. Exceptions map to status codes the way
+// the reference CLI maps them to exit codes (main.cpp:234-246).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+
+#include "kr_internal.hpp"
+
+using namespace kronred;
+using namespace kronred::b200;
+
+namespace kronred {
+Network parse_network_text(const std::string& text);
+}
+
+namespace {
+
+thread_local std::string g_err;
+thread_local double g_pivot = 0.0;
+thread_local int g_node = -1;
+
+}  // namespace
+
+namespace kronred::b200 {
+
+void set_error(const std::string& msg, double pivot, int node) {
+  g_err = msg;
+  g_pivot = pivot;
+  g_node = node;
+}
+
+int status_from_current_exception() {
+  try {
+    throw;
+  } catch (const SolverError& e) {
+    set_error(e.what(), e.smallest_pivot, e.node);
+    return KRG_E_SOLVER;
+  } catch (const ValidationError& e) {
+    set_error(e.what());
+    return KRG_E_VALIDATION;
+  } catch (const CudaError& e) {
+    set_error(e.what());
+    return KRG_E_CUDA;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return KRG_E_INTERNAL;
+  } catch (...) {
+    set_error("unknown error");
+    return KRG_E_INTERNAL;
+  }
+}
+
+}  // namespace kronred::b200
+
+// ---------------------------------------------------------------------------
+// scenario CSV (scenario.cpp:100-212)
+
+struct krg_host_problem {
+  Network net;
+  bool pq = false;
+  std::vector<std::string> ids;
+  std::vector<std::vector<std::pair<int, cx>>> pq_loads;
+  std::vector<double> inj;  // current mode, [L][3n][2]
+  // flat views
+  std::vector<std::uint8_t> phases;
+  std::vector<int32_t> from, to;
+  std::vector<double> ys, sf, st, slackv;
+  std::vector<double> pq_flat;  // [L][3n][2] summed PQ (view only)
+};
+
+struct krg_ctx {
+  std::unique_ptr<Engine> eng;
+};
+
+struct krg_result {
+  ResultData d;
+};
+
+namespace {
+
+std::vector<std::string> split_fields(const std::string& line) {
+  std::vector<std::string> out(1);
+  for (char c : line) {
+    if (c == ',')
+      out.emplace_back();
+    else if (c != '\r')
+      out.back() += c;
+  }
+  for (std::string& f : out) {
+    const auto b = f.find_first_not_of(" \t");
+    const auto e = f.find_last_not_of(" \t");
+    f = b == std::string::npos ? std::string() : f.substr(b, e - b + 1);
+  }
+  return out;
+}
+
+double parse_number(const std::string& s, const std::string& ctx) {
+  try {
+    size_t pos = 0;
+    const double v = std::stod(s, &pos);
+    if (pos != s.size()) throw std::invalid_argument(s);
+    return v;
+  } catch (const std::exception&) {
+    throw ValidationError(ctx + ": bad number '" + s + "'");
+  }
+}
+
+void parse_scenarios(krg_host_problem& hp, const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw ValidationError("cannot open scenario file '" + path + "'");
+  std::string line, header;
+  int lineno = 0;
+  bool have = false;
+  while (std::getline(in, line)) {
+    ++lineno;
+    if (line.empty() || line[0] == '#') continue;
+    header = line;
+    have = true;
+    break;
+  }
+  if (!have) return;  // empty library; rejected when a run starts
+  const auto hf = split_fields(header);
+  if (hf == std::vector<std::string>{"scenario_id", "node_id", "phase", "p_pu", "q_pu"})
+    hp.pq = true;
+  else if (hf == std::vector<std::string>{"scenario_id", "node_id", "phase", "i_re", "i_im"})
+    hp.pq = false;
+  else
+    throw ValidationError("scenario file '" + path + "': unrecognized header '" + header + "'");
+  const int n = hp.net.size();
+  std::map<std::string, size_t> group;
+  while (std::getline(in, line)) {
+    ++lineno;
+    if (line.empty() || line[0] == '#') continue;
+    const std::string ctx = path + ":" + std::to_string(lineno);
+    const auto f = split_fields(line);
+    if (f.size() != 5) throw ValidationError(ctx + ": expected 5 columns, got " + std::to_string(f.size()));
+    auto [it, fresh] = group.try_emplace(f[0], hp.ids.size());
+    if (fresh) {
+      hp.ids.push_back(f[0]);
+      hp.pq_loads.emplace_back();
+      hp.inj.resize(hp.inj.size() + size_t(6 * n), 0.0);
+    }
+    const size_t g = it->second;
+    const int node = int(parse_number(f[1], ctx));
+    int phase = -1;
+    if (f[2] == "a") phase = 0;
+    if (f[2] == "b") phase = 1;
+    if (f[2] == "c") phase = 2;
+    if (phase < 0) throw ValidationError(ctx + ": bad phase '" + f[2] + "' (want a|b|c)");
+    if (node < 0 || node >= n) throw ValidationError(ctx + ": unknown node " + f[1]);
+    if (!hp.net.nodes[size_t(node)].phases.has(phase))
+      throw ValidationError(ctx + ": phase " + f[2] + " absent at node " + f[1]);
+    const double x0 = parse_number(f[3], ctx), x1 = parse_number(f[4], ctx);
+    if (hp.pq) {
+      hp.pq_loads[g].push_back({3 * node + phase, cx{x0, x1}});
+    } else {
+      double* z = &hp.inj[g * size_t(6 * n) + size_t(3 * node + phase) * 2];
+      const cx sum = cx{z[0], z[1]} + cx{x0, x1};
+      z[0] = sum.real();
+      z[1] = sum.imag();
+    }
+  }
+}
+
+void fill_views(krg_host_problem& hp) {
+  const Network& net = hp.net;
+  hp.phases.clear();
+  for (const Node& nd : net.nodes) hp.phases.push_back(nd.phases.bits);
+  hp.slackv.assign(6, 0.0);
+  const int sl = net.slack_id();
+  if (sl >= 0)
+    for (int p = 0; p < 3; ++p) {
+      hp.slackv[size_t(2 * p)] = net.nodes[size_t(sl)].slack_voltage[p].real();
+      hp.slackv[size_t(2 * p + 1)] = net.nodes[size_t(sl)].slack_voltage[p].imag();
+    }
+  for (const Branch& b : net.branches) {
+    hp.from.push_back(b.from);
+    hp.to.push_back(b.to);
+    for (int k = 0; k < 9; ++k) {
+      hp.ys.push_back(b.y_series.m[size_t(k)].real());
+      hp.ys.push_back(b.y_series.m[size_t(k)].imag());
+      hp.sf.push_back(b.shunt_from.m[size_t(k)].real());
+      hp.sf.push_back(b.shunt_from.m[size_t(k)].imag());
+      hp.st.push_back(b.shunt_to.m[size_t(k)].real());
+      hp.st.push_back(b.shunt_to.m[size_t(k)].imag());
+    }
+  }
+  if (hp.pq) {
+    const int n = net.size();
+    hp.pq_flat.assign(hp.ids.size() * size_t(6 * n), 0.0);
+    for (size_t g = 0; g < hp.ids.size(); ++g)
+      for (const auto& ld : hp.pq_loads[g]) {
+        double* z = &hp.pq_flat[g * size_t(6 * n) + size_t(ld.first) * 2];
+        const cx sum = cx{z[0], z[1]} + ld.second;
+        z[0] = sum.real();
+        z[1] = sum.imag();
+      }
+  }
+}
+
+Problem base_problem(const Network& net) {
+  validate_or_throw(net);
+  Problem p;
+  p.net = net;
+  for (const Node& nd : net.nodes) p.mask.push_back(nd.phases.bits);
+  p.slack = net.slack_id();
+  p.y = FlatBlocks::from(assemble_admittance(net));
+  return p;
+}
+
+// scenario_from_currents (scenario.cpp:39-50): zero slack / absent entries
+void zero_invalid(const Network& net, std::vector<double>& inj, int L) {
+  const int n = net.size();
+  for (int l = 0; l < L; ++l)
+    for (const Node& nd : net.nodes)
+      for (int p = 0; p < 3; ++p)
+        if (nd.is_slack || !nd.phases.has(p)) {
+          inj[(size_t(l) * 3 * n + size_t(3 * nd.id + p)) * 2] = 0.0;
+          inj[(size_t(l) * 3 * n + size_t(3 * nd.id + p)) * 2 + 1] = 0.0;
+        }
+}
+
+// scenario_consistent (scenario.cpp:26-31): residual of Y V = I on non-slack
+// present-phase rows, relative to max(1, |I|_inf).
+void check_residual(const Problem& p, const std::vector<double>& inj, const std::vector<double>& volt,
+                    const std::vector<std::string>& ids) {
+  const int n = p.y.n;
+  for (size_t l = 0; l < ids.size(); ++l) {
+    const double* V = volt.data() + l * size_t(6 * n);
+    const double* I = inj.data() + l * size_t(6 * n);
+    std::vector<cx> yv(size_t(3 * n));
+    for (size_t b = 0; b < p.y.row.size(); ++b) {
+      const int i = p.y.row[b], j = p.y.col[b];
+      for (int r = 0; r < 3; ++r) {
+        cx acc{};
+        for (int c = 0; c < 3; ++c)
+          acc += cx{p.y.val[b * 18 + size_t(6 * r + 2 * c)], p.y.val[b * 18 + size_t(6 * r + 2 * c + 1)]} *
+                 cx{V[(3 * j + c) * 2], V[(3 * j + c) * 2 + 1]};
+        yv[size_t(3 * i + r)] += acc;
+      }
+    }
+    double res = 0, inorm = 0;
+    for (int k = 0; k < 3 * n; ++k) inorm = std::max(inorm, std::abs(cx{I[2 * k], I[2 * k + 1]}));
+    for (int i = 0; i < n; ++i) {
+      if (i == p.slack) continue;
+      for (int q = 0; q < 3; ++q)
+        if ((p.mask[size_t(i)] >> q) & 1)
+          res = std::max(res, std::abs(yv[size_t(3 * i + q)] - cx{I[(3 * i + q) * 2], I[(3 * i + q) * 2 + 1]}));
+    }
+    if (!(res <= 1e-10 * std::max(1.0, inorm)))
+      throw SolverError("scenario '" + ids[l] + "' failed the residual check");
+  }
+}
+
+// Engine over a host problem: current mode solves V-hat, PQ mode runs the
+// constant-current fixed point on the device (load_library, scenario.cpp:141-220).
+std::unique_ptr<Engine> engine_from_host(const krg_host_problem& hp, int device) {
+  Problem p = base_problem(hp.net);
+  auto eng = std::make_unique<Engine>(p, device);
+  const int L = int(hp.ids.size());
+  if (L == 0) return eng;
+  std::vector<double> inj, volt;
+  if (hp.pq) {
+    for (size_t g = 0; g < hp.ids.size(); ++g)
+      for (const auto& ld : hp.pq_loads[g])
+        if (ld.first / 3 == p.slack)
+          throw ValidationError("scenario '" + hp.ids[g] + "': load placed at the slack node");
+    // placeholder library (ids for messages); voltages given so no solve runs
+    eng->set_scenarios(hp.ids, std::vector<double>(size_t(L) * 6 * size_t(hp.net.size()), 0.0),
+                       std::vector<double>(size_t(L) * 6 * size_t(hp.net.size()), 0.0));
+    eng->pq_to_currents(hp.pq_loads, inj, volt);
+  } else {
+    inj = hp.inj;
+    zero_invalid(hp.net, inj, L);
+    eng->set_scenarios(hp.ids, inj, {});
+    volt.resize(inj.size());
+    eng->scenario_voltages(volt.data());
+  }
+  check_residual(p, inj, volt, hp.ids);
+  eng->set_scenarios(hp.ids, inj, volt);
+  return eng;
+}
+
+Problem problem_from(const Network& net, const ScenarioLibrary* lib) {
+  Problem p = base_problem(net);
+  if (lib != nullptr) {
+    if (lib->scenarios.empty()) throw ValidationError("scenario library is empty");
+    if (lib->n != net.size()) throw ValidationError("scenario library was built for a different network size");
+    const int n = net.size();
+    p.L = lib->size();
+    for (const Scenario& sc : lib->scenarios) {
+      p.scenario_ids.push_back(sc.id);
+      if (int(sc.injections.size()) != 3 * n || int(sc.voltages.size()) != 3 * n)
+        throw ValidationError("scenario '" + sc.id + "': vectors must have 3n entries");
+      for (const cx& z : sc.injections) {
+        p.injections.push_back(z.real());
+        p.injections.push_back(z.imag());
+      }
+      for (const cx& z : sc.voltages) {
+        p.voltages.push_back(z.real());
+        p.voltages.push_back(z.imag());
+      }
+    }
+  }
+  return p;
+}
+
+ReductionConfig cfg_from_c(const krg_config* c) {
+  ReductionConfig cfg;
+  if (c == nullptr) return cfg;
+  cfg.e_bar = c->e_bar;
+  cfg.objective = c->objective == KRG_OBJ_COMPLEX ? Objective::complex_error : Objective::magnitude;
+  if (c->has_target) cfg.target_reduction = c->target_reduction;
+  cfg.use_delta = c->use_delta != 0;
+  cfg.workers = c->workers;
+  return cfg;
+}
+
+AssignmentState to_public(const HostState& hs) {
+  AssignmentState st;
+  st.n = hs.n;
+  st.slack = hs.slack;
+  st.sup = hs.sup;
+  st.members = hs.members;
+  st.supernodes = hs.supernodes;
+  st.lambda = hs.lambda;
+  return st;
+}
+
+int device_from_env() {
+  if (const char* e = std::getenv("KRONRED_DEVICE")) return std::atoi(e);
+  return -1;  // current device of the calling thread
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C++ drop-in API
+
+namespace kronred {
+
+ScenarioLibrary load_library(const Network& net, const std::string& path) {
+  krg_host_problem hp;
+  hp.net = net;
+  parse_scenarios(hp, path);
+  ScenarioLibrary lib;
+  lib.n = net.size();
+  if (hp.ids.empty()) return lib;
+  auto eng = engine_from_host(hp, device_from_env());
+  const int n = net.size();
+  const Problem& p = eng->problem();
+  for (size_t l = 0; l < hp.ids.size(); ++l) {
+    Scenario sc;
+    sc.id = hp.ids[l];
+    for (int k = 0; k < 3 * n; ++k) {
+      sc.injections.push_back(cx{p.injections[(l * 3 * n + size_t(k)) * 2], p.injections[(l * 3 * n + size_t(k)) * 2 + 1]});
+      sc.voltages.push_back(cx{p.voltages[(l * 3 * n + size_t(k)) * 2], p.voltages[(l * 3 * n + size_t(k)) * 2 + 1]});
+    }
+    lib.scenarios.push_back(std::move(sc));
+  }
+  return lib;
+}
+
+ReductionResult run_reduction(const Network& net, const ScenarioLibrary& lib, const ReductionConfig& cfg,
+                              const IterationObserver& observer) {
+  validate_or_throw(net);
+  if (!(cfg.e_bar >= 0)) throw ConfigError("e_bar must be non-negative");
+  if (cfg.target_reduction && !(*cfg.target_reduction >= 0 && *cfg.target_reduction <= 1))
+    throw ConfigError("target_reduction must lie in [0,1]");
+  Engine eng(problem_from(net, &lib), device_from_env());
+  ResultData rd;
+  Engine::Observer obs;
+  if (observer) obs = [&](const HostState& hs, const TraceRow& row) { observer(to_public(hs), row); };
+  eng.run(cfg, obs, rd);
+  ReductionResult res;
+  res.model = std::move(rd.model);
+  res.trace = std::move(rd.trace);
+  res.state = to_public(rd.state);
+  return res;
+}
+
+KronResult kron_reduce(const BlockMatrix& y, const std::vector<PhaseMask>& phases, const Partition& part) {
+  Problem p;
+  p.y = FlatBlocks::from(y);
+  for (const PhaseMask& m : phases) p.mask.push_back(m.bits);
+  p.slack = -1;
+  Engine eng(p, device_from_env());
+  ReducedModel m;
+  eng.kron(part.reduce, m);
+  std::vector<int> keep = part.keep;
+  std::sort(keep.begin(), keep.end());
+  if (keep != m.kept_ids) throw ValidationError("partition: keep set does not cover the non-reduced nodes");
+  KronResult kr;
+  kr.y_kron = std::move(m.y_kron);
+  kr.kept_ids = std::move(m.kept_ids);
+  kr.kept_phases = std::move(m.kept_phases);
+  return kr;
+}
+
+std::vector<double> model_max_errors(const ReducedModel& model, const Network& net, const ScenarioLibrary& lib) {
+  Engine eng(problem_from(net, &lib), device_from_env());
+  return eng.model_errors(model);
+}
+
+ReducedModel radialize(const ReducedModel& model, const Network& original, const BlockMatrix& y,
+                       const ScenarioLibrary* lib) {
+  Problem p = problem_from(original, lib);
+  p.y = FlatBlocks::from(y);
+  Engine eng(p, device_from_env());
+  ReducedModel out = model;
+  eng.radialize(out, lib != nullptr);
+  return out;
+}
+
+}  // namespace kronred
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+#define KRG_TRY try {
+#define KRG_CATCH \
+  }               \
+  catch (...) { return status_from_current_exception(); }
+
+extern "C" {
+
+const char* krg_last_error(void) { return g_err.c_str(); }
+double krg_last_error_pivot(void) { return g_pivot; }
+int32_t krg_last_error_node(void) { return g_node; }
+const char* krg_version(void) { return "kronred-b200 0.1.0 (sm_100a)"; }
+
+int krg_host_load(const char* net_path, const char* scen_path, krg_host_problem** out) {
+  KRG_TRY
+  auto hp = std::make_unique<krg_host_problem>();
+  std::ifstream f(net_path, std::ios::binary);
+  if (!f) throw ValidationError(std::string("cannot open '") + net_path + "'");
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  hp->net = parse_network_text(ss.str());
+  if (scen_path != nullptr && scen_path[0] != 0) parse_scenarios(*hp, scen_path);
+  fill_views(*hp);
+  *out = hp.release();
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_host_view(const krg_host_problem* p, krg_network* net, int32_t* L, int32_t* pq_mode,
+                  const double** data) {
+  if (p == nullptr) return KRG_E_INTERNAL;
+  net->n_nodes = p->net.size();
+  net->phases = p->phases.data();
+  net->slack = p->net.slack_id();
+  net->slack_voltage = p->slackv.data();
+  net->n_branches = int32_t(p->net.branches.size());
+  net->br_from = p->from.data();
+  net->br_to = p->to.data();
+  net->y_series = p->ys.data();
+  net->shunt_from = p->sf.data();
+  net->shunt_to = p->st.data();
+  if (L) *L = int32_t(p->ids.size());
+  if (pq_mode) *pq_mode = p->pq ? 1 : 0;
+  if (data) *data = p->pq ? p->pq_flat.data() : p->inj.data();
+  return KRG_OK;
+}
+
+const char* krg_host_scenario_id(const krg_host_problem* p, int32_t l) {
+  return (p && l >= 0 && size_t(l) < p->ids.size()) ? p->ids[size_t(l)].c_str() : nullptr;
+}
+
+void krg_host_free(krg_host_problem* p) { delete p; }
+
+int krg_validate(const krg_network* cn) {
+  KRG_TRY
+  validate_or_throw(network_from_c(cn));
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int64_t krg_enumerate_after(const krg_network* cn, const int32_t* ts, const int32_t* tr, int32_t nc,
+                            int32_t* cs, int32_t* cr, int64_t cap) {
+  try {
+    const Network net = network_from_c(cn);
+    validate_or_throw(net);
+    HostState hs;
+    hs.init(net);
+    for (int i = 0; i < nc; ++i) hs.commit(ts[i], tr[i]);
+    std::vector<int> a, b;
+    hs.enumerate(a, b);
+    for (size_t i = 0; i < a.size() && int64_t(i) < cap; ++i) {
+      cs[i] = a[i];
+      cr[i] = b[i];
+    }
+    return int64_t(a.size());
+  } catch (...) {
+    return -int64_t(status_from_current_exception());
+  }
+}
+
+void krg_shard_range(int64_t count, int32_t rank, int32_t world, int64_t* begin, int64_t* end) {
+  // contiguous split, the first (count % world) ranks take one extra
+  // (parallel.cpp:21-29)
+  if (world < 1) world = 1;
+  const int64_t base = count / world, extra = count % world;
+  const int64_t b = rank * base + std::min<int64_t>(rank, extra);
+  *begin = b;
+  *end = b + base + (rank < extra ? 1 : 0);
+}
+
+int32_t krg_merge_best(const double* smice, const int64_t* index, int32_t world) {
+  int32_t best = -1;
+  for (int32_t w = 0; w < world; ++w) {
+    if (index[w] < 0) continue;
+    if (best < 0 || smice[w] < smice[best] || (smice[w] == smice[best] && index[w] < index[best])) best = w;
+  }
+  return best;
+}
+
+int krg_create(const krg_network* cn, const krg_scenarios* scen, int32_t device, krg_ctx** out) {
+  KRG_TRY
+  const Network net = network_from_c(cn);
+  Problem p = base_problem(net);
+  auto ctx = std::make_unique<krg_ctx>();
+  ctx->eng = std::make_unique<Engine>(p, device);
+  if (scen != nullptr && scen->n_scenarios > 0) {
+    const int n = net.size(), L = scen->n_scenarios;
+    std::vector<double> inj(scen->injections, scen->injections + size_t(L) * 6 * n);
+    std::vector<double> volt;
+    std::vector<std::string> ids;
+    for (int l = 0; l < L; ++l) ids.push_back("s" + std::to_string(l));
+    if (scen->voltages != nullptr) {
+      volt.assign(scen->voltages, scen->voltages + size_t(L) * 6 * n);
+    } else {
+      zero_invalid(net, inj, L);
+    }
+    ctx->eng->set_scenarios(ids, inj, volt);
+  }
+  *out = ctx.release();
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_create_from_host(const krg_host_problem* hp, int32_t device, krg_ctx** out) {
+  KRG_TRY
+  auto ctx = std::make_unique<krg_ctx>();
+  ctx->eng = engine_from_host(*hp, device);
+  *out = ctx.release();
+  return KRG_OK;
+  KRG_CATCH
+}
+
+void krg_destroy(krg_ctx* ctx) { delete ctx; }
+
+int krg_set_exchange(krg_ctx* ctx, int32_t rank, int32_t world, krg_exchange_fn fn, void* user) {
+  KRG_TRY
+  ctx->eng->set_exchange(rank, world, fn, user);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int64_t krg_launch_count(const krg_ctx* ctx) { return ctx ? ctx->eng->launches() : 0; }
+
+int krg_scenario_voltages(krg_ctx* ctx, double* out) {
+  KRG_TRY
+  ctx->eng->scenario_voltages(out);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_run_reduction(krg_ctx* ctx, const krg_config* c, krg_observer_fn obs, void* user, krg_result** out) {
+  KRG_TRY
+  auto res = std::make_unique<krg_result>();
+  Engine::Observer o;
+  if (obs)
+    o = [&](const HostState&, const TraceRow& r) {
+      obs(user, r.iteration, r.s, r.r, r.smice, r.max_err.data(), r.supernode_count, r.candidate_count, r.wall_ms);
+    };
+  ctx->eng->run(cfg_from_c(c), o, res->d);
+  *out = res.release();
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_solve(krg_ctx* ctx, const double* inj, int32_t nrhs, double* out) {
+  KRG_TRY
+  ctx->eng->solve(inj, nrhs, out);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_loop_begin(krg_ctx* ctx, const krg_config* c) {
+  KRG_TRY
+  ctx->eng->loop_begin(cfg_from_c(c));
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int64_t krg_loop_candidates(krg_ctx* ctx, int32_t* cs, int32_t* cr, int64_t cap) {
+  try {
+    std::vector<int> a, b;
+    const int64_t C = ctx->eng->loop_candidates(a, b);
+    for (int64_t i = 0; i < C && i < cap; ++i) {
+      cs[i] = a[size_t(i)];
+      cr[i] = b[size_t(i)];
+    }
+    return C;
+  } catch (...) {
+    return -int64_t(status_from_current_exception());
+  }
+}
+
+int krg_loop_score_all(krg_ctx* ctx, double* smice, uint8_t* feasible, double* max_err) {
+  KRG_TRY
+  ctx->eng->loop_score_all(smice, feasible, max_err);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_loop_best(krg_ctx* ctx, krg_best* out, double* max_err) {
+  KRG_TRY
+  ctx->eng->loop_best(out, max_err);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_loop_commit(krg_ctx* ctx, int32_t s, int32_t r) {
+  KRG_TRY
+  ctx->eng->loop_commit(s, r);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_zcols(krg_ctx* ctx, double* out, int64_t cap) {
+  KRG_TRY
+  ctx->eng->zcols(out, cap);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_loop_base(krg_ctx* ctx, double* out) {
+  KRG_TRY
+  ctx->eng->loop_base(out);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_kron_reduce(krg_ctx* ctx, const int32_t* reduce, int32_t m, krg_result** out) {
+  KRG_TRY
+  auto res = std::make_unique<krg_result>();
+  std::vector<int> red(reduce, reduce + m);
+  ctx->eng->kron(red, res->d.model);
+  *out = res.release();
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_radialize(krg_ctx* ctx, krg_result* res, int32_t with_errors) {
+  KRG_TRY
+  ctx->eng->radialize(res->d.model, with_errors != 0);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int32_t krg_result_iterations(const krg_result* r) { return int32_t(r->d.trace.size()); }
+int32_t krg_result_n_scenarios(const krg_result* r) { return int32_t(r->d.model.scenario_ids.size()); }
+
+int krg_result_trace(const krg_result* res, int32_t* s, int32_t* r, double* smice, double* max_err,
+                     int32_t* snc, int32_t* cc, double* wall) {
+  const auto& tr = res->d.trace;
+  for (size_t i = 0; i < tr.size(); ++i) {
+    if (s) s[i] = tr[i].s;
+    if (r) r[i] = tr[i].r;
+    if (smice) smice[i] = tr[i].smice;
+    if (max_err)
+      std::copy(tr[i].max_err.begin(), tr[i].max_err.end(), max_err + i * tr[i].max_err.size());
+    if (snc) snc[i] = tr[i].supernode_count;
+    if (cc) cc[i] = tr[i].candidate_count;
+    if (wall) wall[i] = tr[i].wall_ms;
+  }
+  return KRG_OK;
+}
+
+int32_t krg_result_n_kept(const krg_result* r) { return int32_t(r->d.model.kept_ids.size()); }
+
+int krg_result_kept(const krg_result* r, int32_t* ids, uint8_t* phases) {
+  for (size_t i = 0; i < r->d.model.kept_ids.size(); ++i) {
+    if (ids) ids[i] = r->d.model.kept_ids[i];
+    if (phases) phases[i] = r->d.model.kept_phases[i].bits;
+  }
+  return KRG_OK;
+}
+
+int64_t krg_result_n_blocks(const krg_result* r) { return r->d.model.y_kron.block_count(); }
+
+int krg_result_blocks(const krg_result* r, int32_t* bi, int32_t* bj, double* vals) {
+  const auto& m = r->d.model;
+  size_t k = 0;
+  for (int i = 0; i < m.y_kron.n(); ++i)
+    for (const auto& [j, blk] : m.y_kron.row(i)) {
+      if (bi) bi[k] = m.kept_ids[size_t(i)];
+      if (bj) bj[k] = m.kept_ids[size_t(j)];
+      if (vals)
+        for (int e = 0; e < 9; ++e) {
+          vals[k * 18 + size_t(2 * e)] = blk.m[size_t(e)].real();
+          vals[k * 18 + size_t(2 * e + 1)] = blk.m[size_t(e)].imag();
+        }
+      ++k;
+    }
+  return KRG_OK;
+}
+
+int krg_result_final_max_err(const krg_result* r, double* out) {
+  std::copy(r->d.model.final_max_err.begin(), r->d.model.final_max_err.end(), out);
+  return KRG_OK;
+}
+
+int32_t krg_result_n_clusters(const krg_result* r) { return int32_t(r->d.model.clusters.size()); }
+
+int krg_result_clusters(const krg_result* r, int32_t* sup, int32_t* off, int32_t* members) {
+  size_t k = 0, m = 0;
+  if (off) off[0] = 0;
+  for (const auto& [s, mem] : r->d.model.clusters) {
+    if (sup) sup[k] = s;
+    for (int j : mem) {
+      if (members) members[m] = j;
+      ++m;
+    }
+    ++k;
+    if (off) off[k] = int32_t(m);
+  }
+  return KRG_OK;
+}
+
+int32_t krg_result_n_reinserted(const krg_result* r) { return int32_t(r->d.model.reinserted.size()); }
+
+int krg_result_reinserted(const krg_result* r, int32_t* ids) {
+  std::copy(r->d.model.reinserted.begin(), r->d.model.reinserted.end(), ids);
+  return KRG_OK;
+}
+
+int64_t krg_result_total_candidates(const krg_result* r) { return r->d.total_candidates; }
+
+int krg_result_write_reduced_json(const krg_result* r, const char* path) {
+  KRG_TRY
+  write_reduced_json(r->d.model, path);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_result_write_trace_csv(const krg_result* r, const char* path, int32_t zero_wall) {
+  KRG_TRY
+  std::vector<TraceRow> tr = r->d.trace;
+  if (zero_wall)
+    for (TraceRow& t : tr) t.wall_ms = 0;
+  write_trace_csv(path, tr, r->d.model.scenario_ids, r->d.model.final_max_err);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+void krg_result_free(krg_result* r) { delete r; }
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+"""Regenerate the golden fixtures under tests/golden from the reference build.
+
+Runs oracle/_ref/kronred_ref (the UNMODIFIED reference library compiled by
+oracle/Makefile from /root/reference/proj/src) and stores its inputs/outputs:
+
+  <case>/net.json, scen.csv        inputs (reference writer; current-mode CSV
+                                   whose reload is bit-identical, checked by `gen`)
+  <case>/trace_<tag>.txt           committed (s, r, smice, max_err[]) as IEEE hex
+  <case>/reduced_<tag>.json        reference reduced-model JSON (byte target)
+  <case>/scores_<tag>.txt          per-candidate delta scores, first iterations
+  <case>/solve.txt                 v0, V-hat, every unit-injection solve (hex)
+  <case>/kron_<k>.txt + .reduce    kron_reduce blocks (hex) for random partitions
+
+Usage: python tests/golden/make_golden.py   (needs /root/reference; run here,
+never on the GPU box). Large inputs are gzipped.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import random
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+REF = ROOT / "oracle" / "_ref" / "kronred_ref"
+
+
+def run(*args: str) -> str:
+    p = subprocess.run([str(REF), *args], capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"{args}: {p.stderr}")
+    return p.stdout
+
+
+def gen(case: str, **kw) -> Path:
+    d = HERE / case
+    d.mkdir(exist_ok=True)
+    args = ["gen", "--net", str(d / "net.json"), "--scen", str(d / "scen.csv")]
+    for k, v in kw.items():
+        if k == "pq":
+            pass
+        args += [f"--{k}", str(v)]
+    out = json.loads(run(*args))
+    assert out["roundtrip_bitwise"], case
+    (d / "params.json").write_text(json.dumps(kw, indent=1) + "\n")
+    return d
+
+
+def reduce(d: Path, tag: str, *flags: str, radialize: bool = False) -> dict:
+    args = ["reduce", "--net", str(d / "net.json"), "--scen", str(d / "scen.csv"),
+            "--trace-hex", str(d / f"trace_{tag}.txt"), "--reduced", str(d / f"reduced_{tag}.json"), *flags]
+    if radialize:
+        args.append("--radialize")
+    out = json.loads(run(*args))
+    meta = d / "runs.json"
+    runs = json.loads(meta.read_text()) if meta.exists() else {}
+    runs[tag] = {"flags": list(flags), "radialize": radialize, "iterations": out["iterations"],
+                 "candidates": out["candidates"], "kept": out["kept"]}
+    meta.write_text(json.dumps(runs, indent=1, sort_keys=True) + "\n")
+    return out
+
+
+def scores(d: Path, tag: str, iters: int, *flags: str) -> None:
+    run("scores", "--net", str(d / "net.json"), "--scen", str(d / "scen.csv"), "--iters", str(iters),
+        "--out", str(d / f"scores_{tag}.txt"), *flags)
+
+
+def kron(d: Path, k: int, reduce_set: list[int]) -> None:
+    (d / f"kron_{k}.reduce").write_text(" ".join(map(str, reduce_set)) + "\n")
+    run("kron", "--net", str(d / "net.json"), "--reduce", str(d / f"kron_{k}.reduce"),
+        "--out", str(d / f"kron_{k}.txt"))
+
+
+def gz(path: Path) -> None:
+    with open(path, "rb") as f, gzip.open(str(path) + ".gz", "wb", compresslevel=9) as g:
+        shutil.copyfileobj(f, g)
+    path.unlink()
+
+
+def main() -> None:
+    if not REF.exists():
+        sys.exit("build oracle/_ref first: make -C oracle")
+    # C1: ~100-node acceptance-recipe feeder, 4 scenarios (BASELINE configs[0])
+    d = gen("c1", n=100, seed=1000, L=4, preset="acceptance")
+    for e in ["1e-4", "1e-3", "3e-3", "1e-2"]:
+        reduce(d, f"mag_{e}", "--e-bar", e)
+    reduce(d, "complex_1e-3", "--e-bar", "1e-3", "--objective", "complex")
+    reduce(d, "mag_3e-3_t05", "--e-bar", "3e-3", "--target", "0.5")
+    reduce(d, "rad_1e-2_t06", "--e-bar", "1e-2", "--target", "0.6", radialize=True)
+    scores(d, "mag_1e-3", 3, "--e-bar", "1e-3")
+    scores(d, "complex_1e-3", 2, "--e-bar", "1e-3", "--objective", "complex")
+    rng = random.Random(1)
+    for k in range(3):
+        kron(d, k, sorted(i for i in range(1, 100) if rng.random() < 0.3 + 0.2 * k))
+    # small default-recipe feeder: solver bit checks (every unit column)
+    d = gen("s24", n=24, seed=101, L=2)
+    run("solve", "--net", str(d / "net.json"), "--scen", str(d / "scen.csv"), "--out", str(d / "solve.txt"))
+    reduce(d, "mag_5e-4", "--e-bar", "5e-4")
+    reduce(d, "inf", "--e-bar", "inf")
+    # three-phase-heavy feeder: full 3x3 blocks everywhere
+    d = gen("m40", n=40, seed=77, L=3, frac2=0.003, frac1=0.005)
+    run("solve", "--net", str(d / "net.json"), "--scen", str(d / "scen.csv"), "--out", str(d / "solve.txt"))
+    for e in ["1e-4", "1e-3", "1e-2"]:
+        reduce(d, f"mag_{e}", "--e-bar", e)
+    reduce(d, "complex_1e-3", "--e-bar", "1e-3", "--objective", "complex")
+    scores(d, "mag_1e-3", 4, "--e-bar", "1e-3")
+    rng = random.Random(2)
+    for k in range(3):
+        kron(d, k, sorted(i for i in range(1, 40) if rng.random() < 0.4))
+    # meshed mid-run reduction for radialization (acceptance criterion 7 style)
+    d = gen("r30", n=30, seed=7003, L=2, branching=0.5)
+    reduce(d, "rad_5e-3_t055", "--e-bar", "5e-3", "--target", "0.55", radialize=True)
+    reduce(d, "mag_5e-3_t055", "--e-bar", "5e-3", "--target", "0.55")
+    # constant-PQ scenario CSV (reference default writer)
+    d = gen("pq30", n=30, seed=5, L=3, pq=str(HERE / "pq30" / "scen_pq.csv"))
+    run("reduce", "--net", str(d / "net.json"), "--scen", str(d / "scen_pq.csv"), "--e-bar", "1e-3",
+        "--trace-hex", str(d / "trace_pq_1e-3.txt"), "--reduced", str(d / "reduced_pq_1e-3.json"))
+    run("solve", "--net", str(d / "net.json"), "--scen", str(d / "scen_pq.csv"), "--out", str(d / "solve_pq.txt"))
+    # C2: the 1000-node, 24-scenario benchmark feeder (BASELINE configs[1])
+    d = gen("c2", n=1000, seed=1000, L=24, preset="acceptance")
+    reduce(d, "mag_3e-3", "--e-bar", "3e-3", "--workers", "0")
+    reduce(d, "mag_1e-3", "--e-bar", "1e-3", "--workers", "0")
+    scores(d, "mag_3e-3", 1, "--e-bar", "3e-3")
+    for f in ["net.json", "scen.csv", "trace_mag_3e-3.txt", "trace_mag_1e-3.txt", "reduced_mag_3e-3.json",
+              "reduced_mag_1e-3.json", "scores_mag_3e-3.txt"]:
+        gz(d / f)
+
+
+if __name__ == "__main__":
+    main()

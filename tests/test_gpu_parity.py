@@ -1,0 +1,178 @@
+"""Device parity against the reference build's golden outputs (tests/golden).
+
+Decisions (s, r trajectory, kept ids, clusters) and every committed SMICE /
+max_err are compared BIT FOR BIT; reduced-model JSON byte for byte; Kron
+blocks within 1e-9 of max|Y_kron| (SURVEY §8c parity definition).
+"""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+import paper_2510_19608_b200 as kr
+from golden_io import d2h, h2d, path, read_kron, read_scores, read_solve, read_trace, runs
+
+pytestmark = pytest.mark.gpu
+
+
+def host(case: str, scen: str = "scen.csv") -> kr.HostProblem:
+    return kr.HostProblem(str(path(case, "net.json")), str(path(case, scen)))
+
+
+def cfg_from_flags(flags: list[str]) -> kr.ReductionConfig:
+    c = kr.ReductionConfig()
+    it = iter(flags)
+    for f in it:
+        v = next(it)
+        if f == "--e-bar":
+            c.e_bar = float(v)
+        elif f == "--objective":
+            c.objective = v
+        elif f == "--target":
+            c.target_reduction = float(v)
+    return c
+
+
+def bits(x: float) -> str:
+    return d2h(float(x))
+
+
+def assert_trace(res: kr.Result, case: str, tag: str) -> None:
+    rows, final = read_trace(case, tag)
+    assert len(res.trace) == len(rows), (len(res.trace), len(rows))
+    for got, (s, r, sm, me, snc, cc) in zip(res.trace, rows):
+        assert (got.s, got.r) == (s, r), f"iteration {got.iteration}: {(got.s, got.r)} != {(s, r)}"
+        assert bits(got.smice) == sm, f"iteration {got.iteration} smice {got.smice!r} != {h2d(sm)!r}"
+        assert [bits(e) for e in got.max_err] == me, f"iteration {got.iteration} max_err"
+        assert (got.supernode_count, got.candidate_count) == (snc, cc)
+    assert [bits(e) for e in res.model.final_max_err] == final
+
+
+def test_cdiv_replica_device_matches_host():
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((4096, 4)) * np.exp(rng.uniform(-30, 30, (4096, 4)))
+    q[:64, 2:] = 0.0
+    q[64:128, 0] = np.inf
+    q[128:192, 2] = 1e-310
+    host_out = kr.cdiv_selftest(q, on_device=False)
+    dev_out = kr.cdiv_selftest(q, on_device=True)
+    np.testing.assert_array_equal(host_out.view(np.uint64), dev_out.view(np.uint64))
+
+
+@pytest.mark.parametrize("case", ["s24", "m40"])
+def test_solves_bitwise(case):
+    hp = host(case)
+    ctx = kr.Context(hp)
+    gold = read_solve(case)
+    n = hp.network.size
+    vh = ctx.scenario_voltages()
+    for l in range(len(hp.library.ids)):
+        np.testing.assert_array_equal(vh[l].view(np.uint64), gold[f"vhat{l}"].view(np.uint64))
+    cols = sorted(int(k[1:]) for k in gold if k.startswith("e"))
+    inj = np.zeros((len(cols) + 1, 3 * n), np.complex128)
+    for i, c in enumerate(cols):
+        inj[i, c] = 1.0
+    out = ctx.solve(inj)
+    np.testing.assert_array_equal(out[-1].view(np.uint64), gold["v0"].view(np.uint64))
+    for i, c in enumerate(cols):
+        np.testing.assert_array_equal(out[i].view(np.uint64), gold[f"e{c}"].view(np.uint64))
+
+
+@pytest.mark.parametrize("case,tag,flags", [
+    ("c1", "mag_1e-3", ["--e-bar", "1e-3"]),
+    ("c1", "complex_1e-3", ["--e-bar", "1e-3", "--objective", "complex"]),
+    ("m40", "mag_1e-3", ["--e-bar", "1e-3"]),
+])
+def test_iteration_scores_bitwise(case, tag, flags):
+    gold = read_scores(case, tag)
+    ctx = kr.Context(host(case))
+    ctx.loop_begin(cfg_from_flags(flags))
+    for it in sorted(gold):
+        cands = ctx.loop_candidates()
+        assert cands == [(s, r) for s, r, *_ in gold[it]]
+        sm, fe, me = ctx.loop_score_all()
+        for i, (s, r, feas, smh, meh) in enumerate(gold[it]):
+            assert bool(fe[i]) == feas, (it, s, r)
+            if feas:
+                assert bits(sm[i]) == smh, (it, s, r)
+                assert [bits(x) for x in me[i]] == meh, (it, s, r)
+        idx, s, r, smice, _ = ctx.loop_best()
+        feas_idx = [i for i, g in enumerate(gold[it]) if g[2]]
+        want = min(feas_idx, key=lambda i: (h2d(gold[it][i][3]), i))
+        assert idx == want
+        ctx.loop_commit(s, r)
+
+
+def _golden_runs():
+    out = []
+    for case in ["c1", "s24", "m40", "r30"]:
+        for tag, meta in runs(case).items():
+            out.append((case, tag, meta))
+    return out
+
+
+@pytest.mark.parametrize("case,tag,meta", _golden_runs(), ids=lambda v: v if isinstance(v, str) else None)
+def test_full_run_bitwise(case, tag, meta, tmp_path):
+    hp = host(case)
+    ctx = kr.Context(hp)
+    res = ctx.run_reduction(cfg_from_flags(meta["flags"]))
+    if meta["radialize"]:
+        ctx.radialize(res, with_errors=True)
+    assert_trace(res, case, tag)
+    out = tmp_path / "reduced.json"
+    res.write_reduced_json(str(out))
+    got = json.loads(out.read_text())
+    want = json.loads(path(case, f"reduced_{tag}.json").read_text())
+    assert got["kept"] == want["kept"]
+    assert got["clusters"] == want["clusters"]
+    assert got["reinserted"] == want["reinserted"]
+    assert [e["max_err"] for e in got["errors"]] == [e["max_err"] for e in want["errors"]]
+    gy = {(b["i"], b["j"]): np.array(b["block"]) for b in got["y_kron"]}
+    wy = {(b["i"], b["j"]): np.array(b["block"]) for b in want["y_kron"]}
+    scale = max(np.abs(v).max() for v in wy.values())
+    for k in set(gy) | set(wy):
+        a = gy.get(k, np.zeros((9, 2)))
+        b = wy.get(k, np.zeros((9, 2)))
+        assert np.abs(a - b).max() <= 1e-9 * scale, k
+    # byte identity of the whole file (bit-exact Y_kron)
+    assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
+
+
+@pytest.mark.parametrize("case,k", [("c1", 0), ("c1", 1), ("c1", 2), ("m40", 0), ("m40", 1), ("m40", 2)])
+def test_kron_reduce(case, k):
+    red, want = read_kron(case, k)
+    ctx = kr.Context(host(case))
+    got = ctx.kron_reduce(red).model.y_kron
+    scale = max(np.abs(v).max() for v in want.values())
+    for key in set(got) | set(want):
+        a = got.get(key, np.zeros((3, 3)))
+        b = want.get(key, np.zeros((3, 3)))
+        assert np.abs(a - b).max() <= 1e-9 * scale, key
+    # bit-exact is expected (same elimination order and arithmetic)
+    assert set(got) == set(want)
+    for key in want:
+        np.testing.assert_array_equal(got[key].view(np.uint64), want[key].view(np.uint64))
+
+
+def test_pq_library_and_run():
+    hp = host("pq30", "scen_pq.csv")
+    assert hp.library.pq
+    ctx = kr.Context(hp)
+    gold = read_solve("pq30", "solve_pq.txt")
+    vh = ctx.scenario_voltages()
+    for l in range(3):
+        np.testing.assert_array_equal(vh[l].view(np.uint64), gold[f"vhat{l}"].view(np.uint64))
+    res = ctx.run_reduction(kr.ReductionConfig(e_bar=1e-3))
+    assert_trace(res, "pq30", "pq_1e-3")
+
+
+@pytest.mark.parametrize("tag", ["mag_3e-3", "mag_1e-3"])
+def test_c2_benchmark_feeder_bitwise(tag, tmp_path):
+    ctx = kr.Context(host("c2"))
+    res = ctx.run_reduction(kr.ReductionConfig(e_bar=float(tag.split("_")[1])))
+    assert_trace(res, "c2", tag)
+    out = tmp_path / "r.json"
+    res.write_reduced_json(str(out))
+    assert out.read_text() == path("c2", f"reduced_{tag}.json").read_text()
