@@ -141,6 +141,14 @@ int krg_set_exchange(krg_ctx* ctx, int32_t rank, int32_t world, krg_exchange_fn 
                      void* user);
 /* Number of kernels this context has launched so far. */
 int64_t krg_launch_count(const krg_ctx* ctx);
+/* Per-kernel CUDA-event timing on the launching stream (bench/roofline only):
+ * which = 0 score kernel, 1 base-refresh solve. Sums over launches of the
+ * event time and of the algorithmic flops/bytes. */
+int krg_set_profile(krg_ctx* ctx, int32_t on);
+int krg_kernel_stats(const krg_ctx* ctx, int32_t which, int64_t* launches, double* ms,
+                     double* flops, double* bytes);
+/* Measured unfused FP64 op rate of the device (GFLOP/s), the roofline peak. */
+int krg_fp64_probe(int32_t device, double* gflops);
 /* Device-side V-hat (scenario voltages) as used by the scorer, [L][3n][2]. */
 int krg_scenario_voltages(krg_ctx* ctx, double* out);
 
@@ -188,6 +196,8 @@ int krg_result_clusters(const krg_result* res, int32_t* sup, int32_t* off, int32
 int32_t krg_result_n_reinserted(const krg_result* res);
 int krg_result_reinserted(const krg_result* res, int32_t* ids);
 int64_t krg_result_total_candidates(const krg_result* res);
+/* CUDA-event time (ms) of the whole run on the context's stream. */
+double krg_result_device_ms(const krg_result* res);
 /* Byte-compatible writers (io.cpp:216-265 and io.cpp:338-359). */
 int krg_result_write_reduced_json(const krg_result* res, const char* path);
 int krg_result_write_trace_csv(const krg_result* res, const char* path, int32_t zero_wall);

@@ -127,6 +127,11 @@ _SIGS = [
     ("krg_result_write_reduced_json", C.c_int, [C.c_void_p, C.c_char_p]),
     ("krg_result_write_trace_csv", C.c_int, [C.c_void_p, C.c_char_p, C.c_int32]),
     ("krg_result_free", None, [C.c_void_p]),
+    ("krg_set_profile", C.c_int, [C.c_void_p, C.c_int32]),
+    ("krg_kernel_stats", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("krg_fp64_probe", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
+    ("krg_result_device_ms", C.c_double, [C.c_void_p]),
 ]
 
 
@@ -289,6 +294,13 @@ def merge_best(smice: Sequence[float], index: Sequence[int]) -> int:
     return int(lib().krg_merge_best(_p(s, C.c_double), _p(i, C.c_int64), len(s)))
 
 
+def fp64_probe(device: int = -1) -> float:
+    """Measured unfused FP64 rate (GFLOP/s) — the roofline peak for the scorer."""
+    g = C.c_double()
+    _check(lib().krg_fp64_probe(device, C.byref(g)))
+    return g.value
+
+
 def cdiv_selftest(quads: np.ndarray, on_device: bool) -> np.ndarray:
     q = _f64(quads).reshape(-1, 4)
     out = np.zeros((q.shape[0], 2))
@@ -361,6 +373,7 @@ class Result:
         self.trace = [TraceRow(i + 1, int(s[i]), int(r[i]), float(sm[i]), me[i], int(snc[i]), int(cc[i]),
                                float(wall[i])) for i in range(it)]
         self.total_candidates = int(L.krg_result_total_candidates(handle))
+        self.device_ms = float(L.krg_result_device_ms(handle))
         self.model = self._model()
 
     def _model(self) -> ReducedModel:
@@ -449,6 +462,14 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().krg_launch_count(self._h))
+
+    def set_profile(self, on: bool) -> None:
+        _check(lib().krg_set_profile(self._h, int(on)))
+
+    def kernel_stats(self, which: int) -> dict:
+        n, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        _check(lib().krg_kernel_stats(self._h, which, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by)))
+        return {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
 
     def scenario_voltages(self) -> np.ndarray:
         out = np.zeros(self.L * 3 * self.n * 2)

@@ -564,6 +564,25 @@ int krg_set_exchange(krg_ctx* ctx, int32_t rank, int32_t world, krg_exchange_fn 
 
 int64_t krg_launch_count(const krg_ctx* ctx) { return ctx ? ctx->eng->launches() : 0; }
 
+int krg_set_profile(krg_ctx* ctx, int32_t on) {
+  KRG_TRY
+  ctx->eng->set_profile(on != 0);
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_kernel_stats(const krg_ctx* ctx, int32_t which, int64_t* launches, double* ms, double* flops,
+                     double* bytes) {
+  const KernelStats k = ctx->eng->stats(which);
+  *launches = k.launches;
+  *ms = k.ms;
+  *flops = k.flops;
+  *bytes = k.bytes;
+  return KRG_OK;
+}
+
+double krg_result_device_ms(const krg_result* r) { return r->d.device_ms; }
+
 int krg_scenario_voltages(krg_ctx* ctx, double* out) {
   KRG_TRY
   ctx->eng->scenario_voltages(out);

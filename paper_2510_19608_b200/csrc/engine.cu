@@ -589,6 +589,20 @@ __global__ void prep_kernel(int n, int L, int nphi, const int* prow_node, const 
   }
 }
 
+// Unfused FP64 op-rate probe: 8 independent DMUL->DADD chains per thread.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(int iters, double a, double b, double* sink) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __dadd_rn(__dmul_rn(x[k], a), b);
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) sink[0] = s;
+}
+
 __global__ void selftest_cdiv_kernel(int N, const double* in, double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
@@ -673,8 +687,44 @@ struct Engine::Impl {
   std::vector<int> cs, cr;
   bool loop_active = false;
   bool z_valid = false;
+  // kernel statistics (enabled on demand; CUDA events on the launching stream)
+  bool profile = false;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_run0 = nullptr, ev_run1 = nullptr;
+  KernelStats score_stats{}, solve_stats{};
+  double last_run_ms = 0;
 
   void launched() { ++launches; }
+
+  void ensure_events() {
+    if (!ev_a) {
+      CK(cudaEventCreate(&ev_a));
+      CK(cudaEventCreate(&ev_b));
+      CK(cudaEventCreate(&ev_run0));
+      CK(cudaEventCreate(&ev_run1));
+    }
+  }
+
+  // algorithmic work of one score launch: flops and bytes
+  void score_work(long long c0, long long c1, double& flops, double& bytes) const {
+    long long R = 0;
+    for (int i : hs.supernodes) R += PhaseMask{prob.mask[size_t(i)]}.count();
+    const long long ns = (long long)hs.supernodes.size();
+    std::set<int> cols;
+    flops = 0;
+    for (long long c = c0; c < c1; ++c) {
+      const int q = PhaseMask{prob.mask[size_t(cr[size_t(c)])]}.count();
+      const double Rp = double(R - q);
+      flops += 2.0 * q * Rp + double(L) * ((8.0 * q + 4.0) * Rp + 2.0 * nphi + double(ns - 1));
+      cols.insert(cs[size_t(c)]);
+      cols.insert(cr[size_t(c)]);
+    }
+    long long zc = 0;
+    for (int node : cols) zc += PhaseMask{prob.mask[size_t(node)]}.count();
+    bytes = 16.0 * double(zc) * double(R)          // Z columns of every endpoint over active rows
+            + double(L) * double(R) * (16.0 + 16.0)  // base + cluster min/max
+            + double(c1 - c0) * (8.0 + 48.0 * L)     // candidates + i_agg of r
+            + 4.0 * double(ns) + 16.0 * double(c1 - c0) * L;  // super-node list + outputs
+  }
 
   void upload_elim(DevElim& d, const FlatBlocks& y, const std::vector<std::uint8_t>& mask,
                    const std::vector<int>& elim) {
@@ -814,9 +864,21 @@ struct Engine::Impl {
     a.iagg = d_iagg.p;
     a.base = d_base.p;
     a.L = L;
+    if (profile) CK(cudaEventRecord(ev_a, stream));
     solve_kernel<MODE_BASE><<<L, 512, 0, stream>>>(a);
     launched();
     CK(cudaGetLastError());
+    if (profile) {
+      CK(cudaEventRecord(ev_b, stream));
+      CK(cudaEventSynchronize(ev_b));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+      solve_stats.launches += 1;
+      solve_stats.ms += ms;
+      // forward + backward: per node and RHS ~ (in-degree + 2) Mat3c*Vec3c (54 flops each)
+      solve_stats.flops += double(L) * double(full.h.nsteps) * 3.0 * 54.0;
+      solve_stats.bytes += double(full.h.nsteps) * (3.0 * 144.0) + double(L) * n * 48.0 * 2.0;
+    }
   }
 
   void build_z() {
@@ -931,6 +993,12 @@ struct Engine::Impl {
   }
 
   ~Impl() {
+    if (ev_a) {
+      cudaEventDestroy(ev_a);
+      cudaEventDestroy(ev_b);
+      cudaEventDestroy(ev_run0);
+      cudaEventDestroy(ev_run1);
+    }
     if (h_best) cudaFreeHost(h_best);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -1014,14 +1082,29 @@ struct Engine::Impl {
     a.out_smice = d_psmice.p;
     a.out_maxerr = d_pmaxerr.p;
     const long long pairs = C * L;
+    if (profile) CK(cudaEventRecord(ev_a, stream));
     score_kernel<<<unsigned((pairs + 127) / 128), 128, 0, stream>>>(a);
     launched();
     CK(cudaGetLastError());
+    if (profile) {
+      CK(cudaEventRecord(ev_b, stream));
+      CK(cudaEventSynchronize(ev_b));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+      double f, b;
+      score_work(score_c0, score_c0 + C, f, b);
+      score_stats.launches += 1;
+      score_stats.ms += ms;
+      score_stats.flops += f;
+      score_stats.bytes += b;
+    }
   }
 
   // score [c0,c1) and reduce to the local best; returns (smice, global idx) and max_err in h_best
+  long long score_c0 = 0;
   void score_best(long long c0, long long c1) {
     const long long C = c1 - c0;
+    score_c0 = c0;
     upload_iteration(c0, c1);
     launch_score(C);
     argmin_kernel<<<1, 1024, 0, stream>>>(int(std::max(C, 0LL)), L, cfg.e_bar, c0, d_psmice.p, d_pmaxerr.p,
@@ -1080,6 +1163,14 @@ struct Engine::Impl {
 
 Engine::Engine(const Problem& prob, int device) : impl_(std::make_unique<Impl>(prob, device)) {}
 Engine::~Engine() = default;
+
+void Engine::set_profile(bool on) {
+  impl_->ensure_events();
+  impl_->profile = on;
+  impl_->score_stats = KernelStats{};
+  impl_->solve_stats = KernelStats{};
+}
+KernelStats Engine::stats(int which) const { return which == 0 ? impl_->score_stats : impl_->solve_stats; }
 const Problem& Engine::problem() const { return impl_->prob; }
 std::int64_t Engine::launches() const { return impl_->launches; }
 
@@ -1265,6 +1356,8 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
   Impl& I = *impl_;
   out = ResultData{};
   out.L = I.L;
+  I.ensure_events();
+  CK(cudaEventRecord(I.ev_run0, I.stream));
   I.begin(cfg);
   int iteration = 0;
   while (!I.target_reached()) {
@@ -1314,6 +1407,12 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
   model.scenario_ids = I.prob.scenario_ids;
   model.final_max_err = model_errors(model);
   out.state = I.hs;
+  CK(cudaEventRecord(I.ev_run1, I.stream));
+  CK(cudaEventSynchronize(I.ev_run1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, I.ev_run0, I.ev_run1));
+  out.device_ms = ms;
+  I.last_run_ms = ms;
 }
 
 void Engine::kron(const std::vector<int>& reduce, ReducedModel& model) {
@@ -1433,6 +1532,41 @@ void Engine::radialize(ReducedModel& model, bool with_errors) {
     return this->model_errors(m);
   };
   model = radialize_host(model, impl_->prob.net, kr, with_errors ? &errs : nullptr);
+}
+
+// measured unfused FP64 rate (GFLOP/s, DMUL+DADD counted as 2) on `device`
+extern "C" int krg_fp64_probe(int32_t device, double* gflops) {
+  try {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) throw CudaError("no CUDA device");
+    if (device >= 0) CK(cudaSetDevice(device));
+    int sms = 0, dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf<double> sink;
+    sink.alloc(1);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    fp64_probe_kernel<<<blocks, threads>>>(iters, 0.999999, 1e-7, sink.p);  // warm-up
+    double best = 0;
+    for (int rep = 0; rep < 5; ++rep) {
+      CK(cudaEventRecord(e0));
+      fp64_probe_kernel<<<blocks, threads>>>(iters, 0.999999, 1e-7, sink.p);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::max(best, 2.0 * 8.0 * iters * double(blocks) * threads / (ms * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *gflops = best;
+    return KRG_OK;
+  } catch (...) {
+    return status_from_current_exception();
+  }
 }
 
 // self test hook for the __divdc3 replica (device)

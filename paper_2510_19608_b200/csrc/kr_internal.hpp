@@ -117,6 +117,12 @@ struct ResultData {
   long long total_candidates = 0;
   int L = 0;
   HostState state;
+  double device_ms = 0;  // CUDA-event time of the whole run on the engine stream
+};
+
+struct KernelStats {
+  long long launches = 0;
+  double ms = 0, flops = 0, bytes = 0;  // summed over launches (algorithmic work)
 };
 
 class Engine {
@@ -128,6 +134,8 @@ class Engine {
 
   const Problem& problem() const;
   std::int64_t launches() const;
+  void set_profile(bool on);
+  KernelStats stats(int which) const;  // 0 = score kernel, 1 = base-refresh solve
   void set_exchange(int rank, int world, krg_exchange_fn fn, void* user);
 
   // scenario voltages (V-hat) [L][3n][2]

@@ -71,7 +71,7 @@ ElimSchedule build_schedule(const FlatBlocks& y, const std::vector<std::uint8_t>
       const Key top = heap.top();
       heap.pop();
       const int i = top.second;
-      if (s.eliminated[size_t(i)] || top.first != degree[size_t(i)]) continue;
+      if (!to_elim[size_t(i)] || s.eliminated[size_t(i)] || top.first != degree[size_t(i)]) continue;
       k = i;
       break;
     }
@@ -123,7 +123,7 @@ ElimSchedule build_schedule(const FlatBlocks& y, const std::vector<std::uint8_t>
       }
       row_i.erase(k);
       --degree[size_t(cn[a])];
-      heap.push({degree[size_t(cn[a])], cn[a]});
+      if (to_elim[size_t(cn[a])]) heap.push({degree[size_t(cn[a])], cn[a]});
     }
     row_k.clear();
 
