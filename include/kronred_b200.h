@@ -135,6 +135,9 @@ int krg_create(const krg_network* net, const krg_scenarios* scen, int32_t device
  * the I = -conj(S/V) fixed point with device solves (scenario.cpp:52-98). */
 int krg_create_from_host(const krg_host_problem* p, int32_t device, krg_ctx** out);
 void krg_destroy(krg_ctx* ctx);
+/* Test hook: branch-free scorer sqrt vs IEEE __dsqrt_rn on n device-generated
+ * inputs uniform in [lo, hi); returns the number of bit mismatches. */
+int krg_selftest_sqrt(int64_t n, double lo, double hi, int64_t* mismatches);
 /* Test hook: libgcc __divdc3 replica, in [N][4] = (a,b,c,d) -> out [N][2]. */
 int krg_selftest_cdiv(const double* in, int32_t N, double* out, int32_t on_device);
 int krg_set_exchange(krg_ctx* ctx, int32_t rank, int32_t world, krg_exchange_fn fn,

@@ -132,6 +132,7 @@ _SIGS = [
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("krg_fp64_probe", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
     ("krg_result_device_ms", C.c_double, [C.c_void_p]),
+    ("krg_selftest_sqrt", C.c_int, [C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_int64)]),
 ]
 
 
@@ -299,6 +300,13 @@ def fp64_probe(device: int = -1) -> float:
     g = C.c_double()
     _check(lib().krg_fp64_probe(device, C.byref(g)))
     return g.value
+
+
+def sqrt_selftest(n: int, lo: float, hi: float) -> int:
+    """Bit mismatches of the scorer's branch-free sqrt vs IEEE sqrt (device)."""
+    m = C.c_int64()
+    _check(lib().krg_selftest_sqrt(n, lo, hi, C.byref(m)))
+    return m.value
 
 
 def cdiv_selftest(quads: np.ndarray, on_device: bool) -> np.ndarray:

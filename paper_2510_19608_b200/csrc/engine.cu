@@ -7,26 +7,27 @@
 //                             Serves the anchored factorization
 //                             (solver.cpp:20-117, 168-179) and kron_reduce
 //                             (kron.cpp:34-46, Y_kk - Y_kr Y_rr^-1 Y_rk).
-//   K1s  solve_kernel<MODE>   batched pull-form forward/backward sweeps
-//                             (solver.cpp:119-148): scenario voltages, v0,
-//                             the per-iteration base refresh (reduce.cpp:265)
-//                             and the unit-injection Z columns (reduce.cpp:272).
+//   K1s  csolve_kernel<MODE>  pull-form forward/backward sweeps on the
+//                             present-phase compacted factor staged in shared
+//                             memory (solver.cpp:119-148): scenario voltages,
+//                             v0, the per-iteration base refresh
+//                             (reduce.cpp:265) and the unit-injection Z
+//                             columns (reduce.cpp:272).
 //   K2/3 score_kernel         delta voltage Vc = base + sum_p c_p (Zs_p - Zr_p),
 //                             |Vc|, voltage-margin feasibility and the ordered
 //                             SMICE scan (reduce.cpp:80-123, 194-244).
 //   K4   argmin_kernel        feasibility-masked lexicographic (smice, idx)
 //                             argmin, warp shuffle then block (reduce.cpp:397-404).
-//        commit_kernel        i_agg move + cluster min/max merge (reduce.cpp:336-343).
+//        commit_kernel        i_agg move + cluster bound merge (reduce.cpp:336-343).
 //
 // Exactness: see kr_device.cuh. Every decision is bit-identical to the
-// reference CPU program; the cluster max of |m - vhat_mag_j| over members is
-// evaluated as max(m - min_j, max_j - m), which is exact because rounding is
-// monotone (fl(m - v) is non-increasing in v).
+// reference CPU program (tests/test_gpu_parity.py).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -43,551 +44,38 @@ using dev::C2;
 namespace {
 
 void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess)
-    throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  if (e != cudaSuccess) throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 #define CK(x) ck((x), #x)
 
-// ---------------------------------------------------------------------------
-// device helpers
-
-__device__ __forceinline__ C2 ld2(const double2* p) {
-  const double2 v = *p;
-  return {v.x, v.y};
-}
-__device__ __forceinline__ void st2(double2* p, C2 v) { *p = make_double2(v.x, v.y); }
-
-__device__ __forceinline__ void load_blk(const double2* blocks, int id, C2 m[9]) {
-  if (id < 0) {
-#pragma unroll
-    for (int e = 0; e < 9; ++e) m[e] = {0.0, 0.0};
-    return;
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
   }
-  const double2* p = blocks + size_t(id) * 9;
-#pragma unroll
-  for (int e = 0; e < 9; ++e) m[e] = ld2(p + e);
-}
-
-// Mat3c * Vec3c (complex3.hpp:85-90)
-__device__ __forceinline__ void matvec(const C2 m[9], const C2 x[3], C2 r[3]) {
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    C2 acc = {0.0, 0.0};
-#pragma unroll
-    for (int j = 0; j < 3; ++j) acc = dev::cadd(acc, dev::cmul(m[i * 3 + j], x[j]));
-    r[i] = acc;
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
   }
-}
-
-// Mat3c * Mat3c with exact-zero skip of the left entry (complex3.hpp:76-84)
-__device__ __forceinline__ void matmul(const C2 a[9], const C2 b[9], C2 r[9]) {
-#pragma unroll
-  for (int e = 0; e < 9; ++e) r[e] = {0.0, 0.0};
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const C2 aik = a[i * 3 + k];
-      if (dev::cis0(aik)) continue;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) r[i * 3 + j] = dev::cadd(r[i * 3 + j], dev::cmul(aik, b[k * 3 + j]));
-    }
-}
-
-__device__ __forceinline__ double cabs_dev(C2 z) { return hypot(z.x, z.y); }
-
-// masked_inverse (complex3.cpp:9-61). Pivot magnitudes use hypot (glibc cabs
-// on the host); they only select pivots / gate singularity.
-__device__ bool masked_inverse(const C2 in[9], unsigned mask, C2 out[9], double tol, double& smallest) {
-#pragma unroll
-  for (int e = 0; e < 9; ++e) out[e] = {0.0, 0.0};
-  int idx[3];
-  int k = 0;
-  for (int p = 0; p < 3; ++p)
-    if ((mask >> p) & 1u) idx[k++] = p;
-  smallest = 0.0;
-  if (k == 0) return true;
-  C2 a[3][3], inv[3][3];
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) {
-      a[i][j] = {0.0, 0.0};
-      inv[i][j] = {0.0, 0.0};
-    }
-  for (int i = 0; i < k; ++i) {
-    inv[i][i] = {1.0, 0.0};
-    for (int j = 0; j < k; ++j) a[i][j] = in[idx[i] * 3 + idx[j]];
-  }
-  smallest = __longlong_as_double(0x7ff0000000000000LL);
-  for (int col = 0; col < k; ++col) {
-    int piv = col;
-    double best = cabs_dev(a[col][col]);
-    for (int r = col + 1; r < k; ++r) {
-      const double m = cabs_dev(a[r][col]);
-      if (m > best) {
-        best = m;
-        piv = r;
-      }
-    }
-    smallest = fmin(smallest, best);
-    if (best <= tol) return false;
-    if (piv != col)
-      for (int j = 0; j < 3; ++j) {
-        C2 t = a[piv][j];
-        a[piv][j] = a[col][j];
-        a[col][j] = t;
-        t = inv[piv][j];
-        inv[piv][j] = inv[col][j];
-        inv[col][j] = t;
-      }
-    const C2 d = a[col][col];
-    for (int j = 0; j < k; ++j) {
-      a[col][j] = dev::cdiv(a[col][j], d);
-      inv[col][j] = dev::cdiv(inv[col][j], d);
-    }
-    for (int r = 0; r < k; ++r) {
-      if (r == col) continue;
-      const C2 f = a[r][col];
-      if (dev::cis0(f)) continue;
-      for (int j = 0; j < k; ++j) {
-        a[r][j] = dev::csub(a[r][j], dev::cmul(f, a[col][j]));
-        inv[r][j] = dev::csub(inv[r][j], dev::cmul(f, inv[col][j]));
-      }
-    }
-  }
-  for (int i = 0; i < k; ++i)
-    for (int j = 0; j < k; ++j) out[idx[i] * 3 + idx[j]] = inv[i][j];
-  return true;
-}
-
-// ---------------------------------------------------------------------------
-// K1f: elimination executor
-
-struct ElimDev {
-  int nlevels;
-  const int *step_node, *step_diag;
-  const int *lvl_step_off, *lvl_steps;
-  const int *lvl_slot_off, *lvl_slots, *lvl_slot_step;
-  const int *slot_from, *slot_to;
-  const int *lvl_apply_off, *apply_blk, *apply_off, *apply_slots;
-  const std::uint8_t* mask;
-  double2* blocks;
-  double2* pinv;
-  double2* contrib;
-  double pivot_floor;
-  unsigned long long* fail;  // packed (step << 0) min; fail_info[step] gets pivot
-  double* fail_pivot;
+  ~DBuf() { release(); }
 };
 
-__global__ void __launch_bounds__(1024) elim_factor_kernel(ElimDev e) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int lev = 0; lev < e.nlevels; ++lev) {
-    // A1: structural pseudo-inverse of every pivot at this level
-    const int s0 = e.lvl_step_off[lev], s1 = e.lvl_step_off[lev + 1];
-    for (int i = s0 + tid; i < s1; i += nt) {
-      const int st = e.lvl_steps[i];
-      const int k = e.step_node[st];
-      C2 d[9], pv[9];
-      load_blk(e.blocks, e.step_diag[st], d);
-      double smallest;
-      if (!masked_inverse(d, e.mask[k], pv, e.pivot_floor, smallest)) {
-        const unsigned long long old = atomicMin(e.fail, (unsigned long long)st);
-        (void)old;
-        e.fail_pivot[st] = smallest;
-      }
-      double2* out = e.pinv + size_t(st) * 9;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) st2(out + q, pv[q]);
-    }
-    __syncthreads();
-    // A2: Schur contributions (A_ik pinv_k) A_kj (solver.cpp:94-100)
-    const int q0 = e.lvl_slot_off[lev], q1 = e.lvl_slot_off[lev + 1];
-    for (int i = q0 + tid; i < q1; i += nt) {
-      const int sl = e.lvl_slots[i];
-      const int st = e.lvl_slot_step[i];
-      C2 a[9], p[9], t[9], b[9], c[9];
-      load_blk(e.blocks, e.slot_from[sl], a);
-      load_blk(e.pinv, st, p);
-      matmul(a, p, t);
-      load_blk(e.blocks, e.slot_to[sl], b);
-      matmul(t, b, c);
-      double2* out = e.contrib + size_t(sl) * 9;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) st2(out + q, c[q]);
-    }
-    __syncthreads();
-    // B: ordered apply, block -= contribution in elimination order
-    const int a0 = e.lvl_apply_off[lev], a1 = e.lvl_apply_off[lev + 1];
-    for (int i = a0 + tid; i < a1; i += nt) {
-      const int b = e.apply_blk[i];
-      C2 x[9];
-      load_blk(e.blocks, b, x);
-      for (int j = e.apply_off[i]; j < e.apply_off[i + 1]; ++j) {
-        C2 c[9];
-        load_blk(e.contrib, e.apply_slots[j], c);
-#pragma unroll
-        for (int q = 0; q < 9; ++q) x[q] = dev::csub(x[q], c[q]);
-      }
-      double2* out = e.blocks + size_t(b) * 9;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) st2(out + q, x[q]);
-    }
-    __syncthreads();
-  }
-}
+}  // namespace
+}  // namespace kronred::b200
 
-// ---------------------------------------------------------------------------
-// K1s: batched solves
+#include "kernels_elim.cuh"
+#include "kernels_csolve.cuh"
+#include "kernels_score.cuh"
 
-enum SolveMode { MODE_FULL = 0, MODE_BASE = 1, MODE_ZCOL = 2 };
-
-struct SolveDev {
-  int n, nfw, nbw;
-  const int *step_node, *in_off, *in_node, *in_blk;
-  const int *fw_off, *fw_steps, *bw_off, *bw_steps;
-  const int *cpl_off, *cpl_node, *cpl_to;
-  const double2* blocks;
-  const double2* pinv;
-  int nkept;
-  const int* kept;            // kept node ids
-  const double2* kept_val;    // [nkept][3] preset voltages
-  double2* w;                 // [n][NR][3]
-  int NR;                     // rhs slots in w
-  int nrhs;                   // rhs in this launch
-  int G;                      // rhs per CTA
-  // sources / sinks
-  const double2* rhs_full;    // MODE_FULL: [nrhs][3n] or null (zero)
-  double2* out_full;          // MODE_FULL: [nrhs][3n]
-  const double2* iagg;        // MODE_BASE: [n][L][3]
-  double2* base;              // MODE_BASE: [nphi][L]
-  int L;
-  int nphi;
-  const int* prow_node;       // [nphi]
-  const std::uint8_t* prow_phase;
-  int col0;                   // MODE_ZCOL: first column of this launch
-  const double2* v0p;         // [nphi]
-  double2* zout;              // [ncol][nphi], column-major
-};
-
-template <int MODE>
-__global__ void __launch_bounds__(512) solve_kernel(SolveDev a) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int r0 = blockIdx.x * a.G;
-  const int gc = min(a.G, a.nrhs - r0);
-  if (gc <= 0) return;
-  auto W = [&](int node, int rhs) { return a.w + (size_t(node) * a.NR + rhs) * 3; };
-  // forward: rhs_k = b_k - sum_j A_kj t_j (elimination order), t_k = pinv_k rhs_k
-  for (int lev = 0; lev < a.nfw; ++lev) {
-    const int o0 = a.fw_off[lev], cnt = a.fw_off[lev + 1] - o0;
-    for (int idx = tid; idx < cnt * gc; idx += nt) {
-      const int st = a.fw_steps[o0 + idx / gc];
-      const int rhs = r0 + idx % gc;
-      const int k = a.step_node[st];
-      C2 b[3];
-      if (MODE == MODE_FULL) {
-        if (a.rhs_full) {
-          const double2* src = a.rhs_full + size_t(rhs) * 3 * a.n + size_t(k) * 3;
-          for (int p = 0; p < 3; ++p) b[p] = ld2(src + p);
-        } else {
-          for (int p = 0; p < 3; ++p) b[p] = {0.0, 0.0};
-        }
-      } else if (MODE == MODE_BASE) {
-        const double2* src = a.iagg + (size_t(k) * a.L + rhs) * 3;
-        for (int p = 0; p < 3; ++p) b[p] = ld2(src + p);
-      } else {
-        const int col = a.col0 + rhs;
-        const int cn = a.prow_node[col];
-        const int cp = a.prow_phase[col];
-        for (int p = 0; p < 3; ++p) b[p] = (k == cn && p == cp) ? C2{1.0, 0.0} : C2{0.0, 0.0};
-      }
-      for (int e = a.in_off[st]; e < a.in_off[st + 1]; ++e) {
-        C2 m[9], tj[3], u[3];
-        load_blk(a.blocks, a.in_blk[e], m);
-        const double2* tp = W(a.in_node[e], rhs);
-        for (int p = 0; p < 3; ++p) tj[p] = ld2(tp + p);
-        matvec(m, tj, u);
-        for (int p = 0; p < 3; ++p) b[p] = dev::csub(b[p], u[p]);
-      }
-      C2 pv[9], t[3];
-      load_blk(a.pinv, st, pv);
-      matvec(pv, b, t);
-      double2* wp = W(k, rhs);
-      for (int p = 0; p < 3; ++p) st2(wp + p, t[p]);
-    }
-    __syncthreads();
-  }
-  // boundary values of kept nodes
-  for (int idx = tid; idx < a.nkept * gc; idx += nt) {
-    const int kk = idx / gc, rhs = r0 + idx % gc;
-    double2* wp = W(a.kept[kk], rhs);
-    for (int p = 0; p < 3; ++p) wp[p] = a.kept_val[kk * 3 + p];
-  }
-  __syncthreads();
-  // backward: x_k = t_k - pinv_k (sum_c A_kc x_c), couplings ascending
-  for (int lev = 0; lev < a.nbw; ++lev) {
-    const int o0 = a.bw_off[lev], cnt = a.bw_off[lev + 1] - o0;
-    for (int idx = tid; idx < cnt * gc; idx += nt) {
-      const int st = a.bw_steps[o0 + idx / gc];
-      const int rhs = r0 + idx % gc;
-      const int k = a.step_node[st];
-      C2 acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-      for (int c = a.cpl_off[st]; c < a.cpl_off[st + 1]; ++c) {
-        C2 m[9], xj[3], u[3];
-        load_blk(a.blocks, a.cpl_to[c], m);
-        const double2* xp = W(a.cpl_node[c], rhs);
-        for (int p = 0; p < 3; ++p) xj[p] = ld2(xp + p);
-        matvec(m, xj, u);
-        for (int p = 0; p < 3; ++p) acc[p] = dev::cadd(acc[p], u[p]);
-      }
-      C2 pv[9], corr[3];
-      load_blk(a.pinv, st, pv);
-      matvec(pv, acc, corr);
-      double2* wp = W(k, rhs);
-      for (int p = 0; p < 3; ++p) st2(wp + p, dev::csub(ld2(wp + p), corr[p]));
-    }
-    __syncthreads();
-  }
-  // outputs
-  if (MODE == MODE_FULL) {
-    for (int idx = tid; idx < gc * a.n * 3; idx += nt) {
-      const int g = idx / (a.n * 3), t = idx % (a.n * 3);
-      const int rhs = r0 + g;
-      a.out_full[size_t(rhs) * 3 * a.n + t] = W(t / 3, rhs)[t % 3];
-    }
-  } else if (MODE == MODE_BASE) {
-    for (int idx = tid; idx < a.nphi * gc; idx += nt) {
-      const int rho = idx / gc, rhs = r0 + idx % gc;
-      a.base[size_t(rho) * a.L + rhs] = W(a.prow_node[rho], rhs)[a.prow_phase[rho]];
-    }
-  } else {
-    for (int idx = tid; idx < a.nphi * gc; idx += nt) {
-      const int g = idx / a.nphi, rho = idx % a.nphi;
-      const int rhs = r0 + g;
-      const C2 x = ld2(W(a.prow_node[rho], rhs) + a.prow_phase[rho]);
-      st2(a.zout + size_t(a.col0 + rhs) * a.nphi + rho, dev::csub(x, ld2(a.v0p + rho)));
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2/K3: fused delta contraction + magnitude + feasibility + ordered SMICE
-
-struct ScoreDev {
-  int C;          // candidates in this launch
-  int L;
-  int nphi;
-  int ns;         // active super-nodes
-  const int* cand_s;
-  const int* cand_r;
-  const int* sn;  // active super-nodes, ascending
-  const int* prow_off;
-  const std::uint8_t* mask;
-  const double2* Z;      // [nphi cols][nphi rows]
-  const double2* base;   // [nphi][L]
-  const double* vmin;    // [nphi][L]
-  const double* vmax;    // [nphi][L]
-  const double2* iagg;   // [n][L][3]
-  int objective;
-  const int* mem_off;    // complex objective: CSR members per super-node id
-  const int* mem_list;
-  const double2* vhatp;  // [nphi][L]
-  double* out_smice;     // [C][L]
-  double* out_maxerr;    // [C][L]
-};
-
-__global__ void __launch_bounds__(128) score_kernel(ScoreDev a) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= a.C * a.L) return;
-  const int c = q / a.L, l = q - c * a.L;
-  const int s = a.cand_s[c], r = a.cand_r[c];
-  const unsigned ms = a.mask[s], mr = a.mask[r];
-  const int rs0 = a.prow_off[s], rr0 = a.prow_off[r];
-  // loaded phases of r (reduce.cpp:225-233): c = i_agg[l][3r+p] != 0
-  C2 cv[3];
-  int zs[3], zr[3];
-  int nl = 0;
-  for (int p = 0; p < 3; ++p) {
-    if (!((mr >> p) & 1u)) continue;
-    const C2 cz = ld2(a.iagg + (size_t(r) * a.L + l) * 3 + p);
-    if (dev::cis0(cz)) continue;
-    cv[nl] = cz;
-    zs[nl] = rs0 + __popc(ms & ((1u << p) - 1u));
-    zr[nl] = rr0 + __popc(mr & ((1u << p) - 1u));
-    ++nl;
-  }
-  const size_t nphi = size_t(a.nphi);
-  double smice = 0.0, maxerr = 0.0;
-  for (int k = 0; k < a.ns; ++k) {
-    const int i = a.sn[k];
-    if (i == r) continue;
-    const unsigned mi = a.mask[i];
-    const int ri0 = a.prow_off[i];
-    double cm = 0.0;
-    C2 vrow[3];
-    int t = 0;
-    for (int p = 0; p < 3; ++p) {
-      if (!((mi >> p) & 1u)) continue;
-      const int rho = ri0 + t;
-      ++t;
-      C2 v = ld2(a.base + size_t(rho) * a.L + l);
-      for (int j = 0; j < nl; ++j) {
-        const C2 za = ld2(a.Z + size_t(zs[j]) * nphi + rho);
-        const C2 zb = ld2(a.Z + size_t(zr[j]) * nphi + rho);
-        const double dr = dev::dsub(za.x, zb.x), di = dev::dsub(za.y, zb.y);
-        v.x = dev::dadd(v.x, dev::dsub(dev::dmul(cv[j].x, dr), dev::dmul(cv[j].y, di)));
-        v.y = dev::dadd(v.y, dev::dadd(dev::dmul(cv[j].x, di), dev::dmul(cv[j].y, dr)));
-      }
-      vrow[p] = v;
-      const double m = dev::dsqrt(dev::dadd(dev::dmul(v.x, v.x), dev::dmul(v.y, v.y)));
-      double lo = a.vmin[size_t(rho) * a.L + l], hi = a.vmax[size_t(rho) * a.L + l];
-      if (i == s && ((mr >> p) & 1u)) {
-        const int rr = rr0 + __popc(mr & ((1u << p) - 1u));
-        lo = fmin(lo, a.vmin[size_t(rr) * a.L + l]);
-        hi = fmax(hi, a.vmax[size_t(rr) * a.L + l]);
-      }
-      const double em = fmax(dev::dsub(m, lo), dev::dsub(hi, m));
-      maxerr = fmax(maxerr, em);
-      cm = fmax(cm, em);
-    }
-    if (a.objective == KRG_OBJ_COMPLEX) {
-      // objective entries are complex distances (reduce.cpp:102-106)
-      cm = 0.0;
-      for (int pass = 0; pass < (i == s ? 2 : 1); ++pass) {
-        const int owner = pass == 0 ? i : r;
-        for (int e = a.mem_off[owner]; e < a.mem_off[owner + 1]; ++e) {
-          const int j = a.mem_list[e];
-          const unsigned mj = a.mask[j];
-          int tj = 0;
-          for (int p = 0; p < 3; ++p) {
-            if (!((mj >> p) & 1u)) continue;
-            const C2 vh = ld2(a.vhatp + size_t(a.prow_off[j] + tj) * a.L + l);
-            ++tj;
-            const double dr = dev::dsub(vrow[p].x, vh.x), di = dev::dsub(vrow[p].y, vh.y);
-            const double eo = dev::dsqrt(dev::dadd(dev::dmul(dr, dr), dev::dmul(di, di)));
-            cm = fmax(cm, eo);
-          }
-        }
-      }
-    }
-    smice = dev::dadd(smice, cm);
-  }
-  a.out_smice[q] = smice;
-  a.out_maxerr[q] = maxerr;
-}
-
-// ---------------------------------------------------------------------------
-// K4: per-candidate scenario sum + feasibility, lexicographic argmin
-
-struct BestRec {
-  double smice;
-  long long idx;
-};
-
-__device__ __forceinline__ bool better(double s1, long long i1, double s2, long long i2) {
-  if (i1 < 0) return false;
-  if (i2 < 0) return true;
-  return s1 < s2 || (s1 == s2 && i1 < i2);
-}
-
-__global__ void __launch_bounds__(1024) argmin_kernel(int C, int L, double e_bar, long long c_base,
-                                                      const double* smice_l, const double* maxerr_l,
-                                                      double* out /* [2 + L] */) {
-  __shared__ double ss[32];
-  __shared__ long long si[32];
-  double bs = __longlong_as_double(0x7ff0000000000000LL);
-  long long bi = -1;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    bool feasible = true;
-    double sum = 0.0;
-    for (int l = 0; l < L; ++l) {
-      feasible = feasible && !(maxerr_l[size_t(c) * L + l] > e_bar);
-      sum = dev::dadd(sum, smice_l[size_t(c) * L + l]);
-    }
-    if (feasible && better(sum, c, bs, bi)) {
-      bs = sum;
-      bi = c;
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    const double os = __shfl_down_sync(0xffffffffu, bs, off);
-    const long long oi = __shfl_down_sync(0xffffffffu, bi, off);
-    if (better(os, oi, bs, bi)) {
-      bs = os;
-      bi = oi;
-    }
-  }
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (lane == 0) {
-    ss[warp] = bs;
-    si[warp] = bi;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x / 32;
-    bs = lane < nw ? ss[lane] : __longlong_as_double(0x7ff0000000000000LL);
-    bi = lane < nw ? si[lane] : -1;
-    for (int off = 16; off > 0; off >>= 1) {
-      const double os = __shfl_down_sync(0xffffffffu, bs, off);
-      const long long oi = __shfl_down_sync(0xffffffffu, bi, off);
-      if (better(os, oi, bs, bi)) {
-        bs = os;
-        bi = oi;
-      }
-    }
-    if (lane == 0) {
-      si[0] = bi;
-      ss[0] = bs;
-    }
-  }
-  __syncthreads();
-  bi = si[0];
-  if (threadIdx.x == 0) {
-    out[0] = ss[0];
-    out[1] = __longlong_as_double(bi < 0 ? -1 : bi + c_base);
-  }
-  for (int l = threadIdx.x; l < L; l += blockDim.x)
-    out[2 + l] = bi < 0 ? 0.0 : maxerr_l[size_t(bi) * L + l];
-}
-
-// commit: i_agg[s] += i_agg[r], i_agg[r] = 0 (reduce.cpp:336-343); the
-// absorbing cluster's per-phase min/max of member |V-hat| takes r's.
-__global__ void commit_kernel(int s, int r, int L, unsigned ms, unsigned mr, int rs0, int rr0,
-                              double2* iagg, double* vmin, double* vmax) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= L) return;
-  for (int p = 0; p < 3; ++p) {
-    double2* ps = iagg + (size_t(s) * L + l) * 3 + p;
-    double2* pr = iagg + (size_t(r) * L + l) * 3 + p;
-    st2(ps, dev::cadd(ld2(ps), ld2(pr)));
-    *pr = make_double2(0.0, 0.0);
-    if ((mr >> p) & 1u) {
-      const size_t a = size_t(rs0 + __popc(ms & ((1u << p) - 1u))) * L + l;
-      const size_t b = size_t(rr0 + __popc(mr & ((1u << p) - 1u))) * L + l;
-      vmin[a] = fmin(vmin[a], vmin[b]);
-      vmax[a] = fmax(vmax[a], vmax[b]);
-    }
-  }
-}
-
-// scenario data prep: present-row V-hat, |V-hat| (kernels::magnitude order),
-// initial cluster bounds and the [n][L][3] aggregated injections.
-__global__ void prep_kernel(int n, int L, int nphi, const int* prow_node, const std::uint8_t* prow_phase,
-                            const double2* vhat_full, const double2* inj_full, double2* vhatp,
-                            double* vmag, double* vmin, double* vmax, double2* iagg) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < nphi * L) {
-    const int rho = idx / L, l = idx % L;
-    const C2 v = ld2(vhat_full + size_t(l) * 3 * n + size_t(prow_node[rho]) * 3 + prow_phase[rho]);
-    const double m = dev::dsqrt(dev::dadd(dev::dmul(v.x, v.x), dev::dmul(v.y, v.y)));
-    st2(vhatp + idx, v);
-    vmag[idx] = m;
-    vmin[idx] = m;
-    vmax[idx] = m;
-  }
-  if (idx < n * L * 3) {
-    const int node = idx / (L * 3), rem = idx % (L * 3), l = rem / 3, p = rem % 3;
-    iagg[idx] = inj_full[size_t(l) * 3 * n + size_t(node) * 3 + p];
-  }
-}
+namespace kronred::b200 {
+namespace {
 
 // Unfused FP64 op-rate probe: 8 independent DMUL->DADD chains per thread.
 __global__ void __launch_bounds__(256) fp64_probe_kernel(int iters, double a, double b, double* sink) {
@@ -611,32 +99,12 @@ __global__ void selftest_cdiv_kernel(int N, const double* in, double* out) {
   out[2 * i + 1] = r.y;
 }
 
-// ---------------------------------------------------------------------------
-// device buffers
-
-template <class T>
-struct DBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  void alloc(size_t count) {
-    if (count <= n && p) return;
-    release();
-    if (count == 0) count = 1;
-    CK(cudaMalloc(&p, count * sizeof(T)));
-    n = count;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  ~DBuf() { release(); }
-};
+int gcd_int(int a, int b) { return b == 0 ? a : gcd_int(b, a % b); }
 
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Engine implementation
+// one elimination: schedule, device work lists, factor, compacted solve program
 
 struct DevElim {
   ElimSchedule h;
@@ -646,15 +114,24 @@ struct DevElim {
   DBuf<std::uint8_t> mask;
   DBuf<unsigned long long> fail;
   DBuf<double> fail_pivot;
+  // present-phase compacted factor + level program for csolve_kernel
+  CProg prog{};
+  DBuf<int> meta;
+  DBuf<long long> gsrc;
+  DBuf<double2> cfac;
+  DBuf<int> prow_off;
+  std::vector<int> xoff;
+  int smem_bytes = 0, smem_factor = 0;
   const int* P(int which) const { return ints.p + off[size_t(which)]; }
 };
 
 enum IntArr {
   A_STEP_NODE, A_STEP_DIAG, A_LVL_STEP_OFF, A_LVL_STEPS, A_LVL_SLOT_OFF, A_LVL_SLOTS,
   A_LVL_SLOT_STEP, A_SLOT_FROM, A_SLOT_TO, A_LVL_APPLY_OFF, A_APPLY_BLK, A_APPLY_OFF,
-  A_APPLY_SLOTS, A_IN_OFF, A_IN_NODE, A_IN_BLK, A_FW_OFF, A_FW_STEPS, A_BW_OFF, A_BW_STEPS,
-  A_CPL_OFF, A_CPL_NODE, A_CPL_TO, A_KEPT, A_COUNT
+  A_APPLY_SLOTS, A_COUNT
 };
+
+constexpr int kTabPad = 64;  // row-table padding >= largest score_rows tile (S*T)
 
 struct Engine::Impl {
   Problem prob;
@@ -662,6 +139,7 @@ struct Engine::Impl {
   cudaStream_t stream = nullptr;
   long long launches = 0;
   int n = 0, L = 0, nphi = 0;
+  int optin_smem = 0;
   std::vector<int> prow_off, prow_node;
   std::vector<std::uint8_t> prow_phase;
   DBuf<int> d_prow_off, d_prow_node;
@@ -669,14 +147,34 @@ struct Engine::Impl {
   DBuf<double2> d_yin;        // assembled Y blocks (input, resident)
   double pivot_floor = 0;
   DevElim full;               // anchored factorization of Y
-  DBuf<double2> d_w;          // solve scratch
-  DBuf<double2> d_inj, d_vhat, d_v0, d_v0p, d_vhatp, d_iagg, d_base, d_Z;
-  DBuf<double> d_vmag, d_vmin, d_vmax;
+  DBuf<double2> d_inj, d_vhat, d_v0, d_v0p, d_vhatp, d_iagg, d_bv, d_Z, d_slackv;
   std::vector<double> h_vhat;  // [L][3n][2]
-  DBuf<int> d_cs, d_cr, d_sn, d_memoff, d_memlist;
-  DBuf<double> d_psmice, d_pmaxerr, d_best;
+  // per-iteration inputs (pinned staging)
+  DBuf<int4> d_cand;
+  DBuf<unsigned> d_snt;
+  DBuf<int> d_snid, d_memoff, d_memlist;
+  int4* h_cand = nullptr;
+  unsigned* h_snt = nullptr;
+  // magnitude path: active-row table + candidates grouped by |phi(r)|
+  DBuf<unsigned> d_tab;
+  DBuf<int> d_cidx;
+  unsigned* h_tab = nullptr;
+  int* h_cidx = nullptr;
+  std::vector<int> tab_of_node;
+  int R = 0;
+  int grp_off[4] = {0, 0, 0, 0};
+  std::vector<int> sn_pos;     // compact index of each active super-node
+  DBuf<double> d_psmice, d_pmaxerr, d_pcand, d_best;
+  bool use_tiles = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) != "rows";
+
+  // threads per scorer CTA: a multiple of L (whole candidates) and of 32
+  int score_cta_threads() const {
+    int P = L * (32 / gcd_int(L, 32));
+    if (P > 256) P = (L + 31) / 32 * 32;  // one candidate per CTA, idle tail lanes
+    if (P > 512) throw ConfigError("more than 512 scenarios are not supported by the scorer CTA layout");
+    return P;
+  }
   double* h_best = nullptr;    // pinned [2 + L]
-  DBuf<double2> d_slackv;
   // multi-GPU
   int rank = 0, world = 1;
   krg_exchange_fn xfn = nullptr;
@@ -686,12 +184,11 @@ struct Engine::Impl {
   HostState hs;
   std::vector<int> cs, cr;
   bool loop_active = false;
-  bool z_valid = false;
   // kernel statistics (enabled on demand; CUDA events on the launching stream)
   bool profile = false;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_run0 = nullptr, ev_run1 = nullptr;
   KernelStats score_stats{}, solve_stats{};
-  double last_run_ms = 0;
+  long long score_c0 = 0;
 
   void launched() { ++launches; }
 
@@ -702,6 +199,14 @@ struct Engine::Impl {
       CK(cudaEventCreate(&ev_run0));
       CK(cudaEventCreate(&ev_run1));
     }
+  }
+
+  float event_ms() {
+    CK(cudaEventRecord(ev_b, stream));
+    CK(cudaEventSynchronize(ev_b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+    return ms;
   }
 
   // algorithmic work of one score launch: flops and bytes
@@ -720,29 +225,31 @@ struct Engine::Impl {
     }
     long long zc = 0;
     for (int node : cols) zc += PhaseMask{prob.mask[size_t(node)]}.count();
-    bytes = 16.0 * double(zc) * double(R)          // Z columns of every endpoint over active rows
-            + double(L) * double(R) * (16.0 + 16.0)  // base + cluster min/max
-            + double(c1 - c0) * (8.0 + 48.0 * L)     // candidates + i_agg of r
-            + 4.0 * double(ns) + 16.0 * double(c1 - c0) * L;  // super-node list + outputs
+    bytes = 16.0 * double(zc) * double(R)               // Z columns of every endpoint over active rows
+            + double(L) * double(R) * 32.0              // base + cluster min/max
+            + double(c1 - c0) * (16.0 + 48.0 * L)       // candidates + i_agg of r
+            + 4.0 * double(ns) + 16.0 * double(c1 - c0) * L;  // super-node table + outputs
   }
 
+  // ---- elimination schedules -----------------------------------------------
+
   void upload_elim(DevElim& d, const FlatBlocks& y, const std::vector<std::uint8_t>& mask,
-                   const std::vector<int>& elim) {
+                   const std::vector<int>& elim, bool with_solve = true) {
     d.h = build_schedule(y, mask, elim);
     const ElimSchedule& h = d.h;
     const std::vector<const std::vector<int>*> arrs = {
         &h.step_node, &h.step_diag, &h.lvl_step_off, &h.lvl_steps, &h.lvl_slot_off, &h.lvl_slots,
         &h.lvl_slot_step, &h.slot_from, &h.slot_to, &h.lvl_apply_off, &h.apply_blk, &h.apply_off,
-        &h.apply_slots, &h.in_off, &h.in_node, &h.in_blk, &h.fw_off, &h.fw_steps, &h.bw_off,
-        &h.bw_steps, &h.cpl_off, &h.cpl_node, &h.cpl_to, &h.kept};
+        &h.apply_slots};
     d.off.assign(A_COUNT + 1, 0);
     for (int i = 0; i < A_COUNT; ++i) d.off[size_t(i) + 1] = d.off[size_t(i)] + arrs[size_t(i)]->size();
     std::vector<int> packed(d.off[A_COUNT]);
     for (int i = 0; i < A_COUNT; ++i)
       std::copy(arrs[size_t(i)]->begin(), arrs[size_t(i)]->end(), packed.begin() + long(d.off[size_t(i)]));
     d.ints.alloc(packed.size());
-    CK(cudaMemcpyAsync(d.ints.p, packed.data(), packed.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
-    d.blocks.alloc(size_t(h.nblocks) * 9);
+    if (!packed.empty())
+      CK(cudaMemcpyAsync(d.ints.p, packed.data(), packed.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+    d.blocks.alloc(size_t(std::max(h.nblocks, 1)) * 9);
     d.pinv.alloc(size_t(std::max(h.nsteps, 1)) * 9);
     d.contrib.alloc(size_t(std::max(h.nslots, 1)) * 9);
     d.mask.alloc(mask.size());
@@ -750,19 +257,123 @@ struct Engine::Impl {
     d.fail.alloc(1);
     d.fail_pivot.alloc(size_t(std::max(h.nsteps, 1)));
     CK(cudaStreamSynchronize(stream));
+    if (with_solve) build_compact(d);
   }
 
-  // K1f on the device: blocks <- input, fill <- 0, then the level executor.
+  // Host: present-phase layout of the factor and the packed level program.
+  void build_compact(DevElim& d) {
+    const ElimSchedule& h = d.h;
+    const int nn = h.n;
+    d.xoff.assign(size_t(nn) + 1, 0);
+    for (int i = 0; i < nn; ++i) d.xoff[size_t(i) + 1] = d.xoff[size_t(i)] + __builtin_popcount(h.mask[size_t(i)]);
+    std::vector<int> st_x, st_m, st_mask, st_node, st_pinv, in_off{0}, in_x, in_m, in_blk, cp_off{0}, cp_x, cp_m,
+        cp_blk, kept_x, kept_m, kept_i;
+    std::vector<long long> g;
+    auto present = [&](int node, int* idx) {
+      int k = 0;
+      for (int p = 0; p < 3; ++p)
+        if ((h.mask[size_t(node)] >> p) & 1) idx[k++] = p;
+      return k;
+    };
+    auto gather_block = [&](long long base9, bool is_pinv, int rn, int cn) {
+      int ri[3], ci[3];
+      const int mr = present(rn, ri), mc = present(cn, ci);
+      const int off = int(g.size());
+      for (int i = 0; i < mr; ++i)
+        for (int j = 0; j < mc; ++j)
+          g.push_back(base9 < 0 ? -1 : (((base9 + ri[i] * 3 + ci[j]) << 1) | (is_pinv ? 1 : 0)));
+      return off;
+    };
+    for (int st = 0; st < h.nsteps; ++st) {
+      const int k = h.step_node[size_t(st)];
+      st_x.push_back(d.xoff[size_t(k)]);
+      st_m.push_back(__builtin_popcount(h.mask[size_t(k)]));
+      st_mask.push_back(h.mask[size_t(k)]);
+      st_node.push_back(k);
+      st_pinv.push_back(gather_block((long long)st * 9, true, k, k));
+      for (int e = h.in_off[size_t(st)]; e < h.in_off[size_t(st) + 1]; ++e) {
+        const int j = h.in_node[size_t(e)], b = h.in_blk[size_t(e)];
+        in_x.push_back(d.xoff[size_t(j)]);
+        in_m.push_back(__builtin_popcount(h.mask[size_t(j)]));
+        in_blk.push_back(gather_block(b < 0 ? -1 : (long long)b * 9, false, k, j));
+      }
+      in_off.push_back(int(in_x.size()));
+      for (int e = h.cpl_off[size_t(st)]; e < h.cpl_off[size_t(st) + 1]; ++e) {
+        const int j = h.cpl_node[size_t(e)], b = h.cpl_to[size_t(e)];
+        cp_x.push_back(d.xoff[size_t(j)]);
+        cp_m.push_back(__builtin_popcount(h.mask[size_t(j)]));
+        cp_blk.push_back(gather_block(b < 0 ? -1 : (long long)b * 9, false, k, j));
+      }
+      cp_off.push_back(int(cp_x.size()));
+    }
+    for (size_t kk = 0; kk < h.kept.size(); ++kk) {
+      kept_x.push_back(d.xoff[size_t(h.kept[kk])]);
+      kept_m.push_back(__builtin_popcount(h.mask[size_t(h.kept[kk])]));
+      kept_i.push_back(int(kk));
+    }
+    std::vector<int> meta;
+    auto put = [&](const std::vector<int>& v) {
+      const int o = int(meta.size());
+      meta.insert(meta.end(), v.begin(), v.end());
+      return o;
+    };
+    CProg P{};
+    P.st_x = put(st_x);
+    P.st_m = put(st_m);
+    P.st_mask = put(st_mask);
+    P.st_node = put(st_node);
+    P.st_pinv = put(st_pinv);
+    P.in_off = put(in_off);
+    P.in_x = put(in_x);
+    P.in_m = put(in_m);
+    P.in_blk = put(in_blk);
+    P.cp_off = put(cp_off);
+    P.cp_x = put(cp_x);
+    P.cp_m = put(cp_m);
+    P.cp_blk = put(cp_blk);
+    P.fw_off = put(h.fw_off);
+    P.fw = put(h.fw_steps);
+    P.bw_off = put(h.bw_off);
+    P.bw = put(h.bw_steps);
+    P.kept_x = put(kept_x);
+    P.kept_m = put(kept_m);
+    P.kept_i = put(kept_i);
+    P.nsteps = h.nsteps;
+    P.nfw = h.nsteps ? h.nfw : 0;
+    P.nbw = h.nsteps ? h.nbw : 0;
+    P.nkept = int(h.kept.size());
+    P.nmeta = int(meta.size());
+    P.ncf = int(g.size());
+    P.nphi = d.xoff[size_t(nn)];
+    d.prog = P;
+    d.meta.alloc(meta.size());
+    if (!meta.empty())
+      CK(cudaMemcpyAsync(d.meta.p, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+    d.gsrc.alloc(g.size());
+    if (!g.empty())
+      CK(cudaMemcpyAsync(d.gsrc.p, g.data(), g.size() * sizeof(long long), cudaMemcpyHostToDevice, stream));
+    d.cfac.alloc(g.size());
+    d.prow_off.alloc(d.xoff.size());
+    CK(cudaMemcpyAsync(d.prow_off.p, d.xoff.data(), d.xoff.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+    const size_t xb = size_t(P.nphi) * sizeof(double2);
+    const size_t all = xb + size_t(P.ncf) * sizeof(double2) + size_t(P.nmeta) * sizeof(int);
+    if (xb > size_t(optin_smem)) throw Error("solution vector does not fit in shared memory");
+    d.smem_factor = all <= size_t(optin_smem) ? 1 : 0;
+    d.smem_bytes = int(d.smem_factor ? all : xb);
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  // K1f on the device: blocks <- input, fill <- 0, then the level executor,
+  // then the present-phase compaction of the factor.
   void factorize(DevElim& d, const double2* d_input, double floor) {
     const ElimSchedule& h = d.h;
     if (h.n_input > 0)
-      CK(cudaMemcpyAsync(d.blocks.p, d_input, size_t(h.n_input) * 9 * sizeof(double2),
-                         cudaMemcpyDeviceToDevice, stream));
+      CK(cudaMemcpyAsync(d.blocks.p, d_input, size_t(h.n_input) * 9 * sizeof(double2), cudaMemcpyDeviceToDevice,
+                         stream));
     if (h.nblocks > h.n_input)
-      CK(cudaMemsetAsync(d.blocks.p + size_t(h.n_input) * 9, 0,
-                         size_t(h.nblocks - h.n_input) * 9 * sizeof(double2), stream));
-    const unsigned long long none = ~0ull;
-    CK(cudaMemcpyAsync(d.fail.p, &none, sizeof(none), cudaMemcpyHostToDevice, stream));
+      CK(cudaMemsetAsync(d.blocks.p + size_t(h.n_input) * 9, 0, size_t(h.nblocks - h.n_input) * 9 * sizeof(double2),
+                         stream));
+    CK(cudaMemsetAsync(d.fail.p, 0xff, sizeof(unsigned long long), stream));
     if (h.nlevels > 0) {
       ElimDev e;
       e.nlevels = h.nlevels;
@@ -800,102 +411,71 @@ struct Engine::Impl {
       char buf[64];
       std::snprintf(buf, sizeof buf, "%.3e", piv);
       throw SolverError("singular present-phase diagonal while eliminating node " + std::to_string(node) +
-                            " (smallest pivot " + buf + ", " + std::to_string(h.nsteps - int(failed)) +
-                            " of " + std::to_string(h.nsteps) + " eliminations left)",
+                            " (smallest pivot " + buf + ", " + std::to_string(h.nsteps - int(failed)) + " of " +
+                            std::to_string(h.nsteps) + " eliminations left)",
                         piv, node);
     }
-  }
-
-  SolveDev solve_args(DevElim& d, const double2* kept_val, int NR) {
-    const ElimSchedule& h = d.h;
-    SolveDev a{};
-    a.n = h.n;
-    a.nfw = h.nfw;
-    a.nbw = h.nbw;
-    a.step_node = d.P(A_STEP_NODE);
-    a.in_off = d.P(A_IN_OFF);
-    a.in_node = d.P(A_IN_NODE);
-    a.in_blk = d.P(A_IN_BLK);
-    a.fw_off = d.P(A_FW_OFF);
-    a.fw_steps = d.P(A_FW_STEPS);
-    a.bw_off = d.P(A_BW_OFF);
-    a.bw_steps = d.P(A_BW_STEPS);
-    a.cpl_off = d.P(A_CPL_OFF);
-    a.cpl_node = d.P(A_CPL_NODE);
-    a.cpl_to = d.P(A_CPL_TO);
-    a.blocks = d.blocks.p;
-    a.pinv = d.pinv.p;
-    a.nkept = int(h.kept.size());
-    a.kept = d.P(A_KEPT);
-    a.kept_val = kept_val;
-    d_w.alloc(size_t(h.n) * size_t(NR) * 3);
-    a.w = d_w.p;
-    a.NR = NR;
-    return a;
-  }
-
-  // Full anchored solves: rhs [nrhs][3n] (device, may be null) -> out [nrhs][3n]
-  void solve_full(DevElim& d, const double2* kept_val, const double2* rhs, int nrhs, double2* out) {
-    const int chunk = 1024;
-    for (int r0 = 0; r0 < nrhs; r0 += chunk) {
-      const int nr = std::min(chunk, nrhs - r0);
-      SolveDev a = solve_args(d, kept_val, nr);
-      a.nrhs = nr;
-      a.G = 4;
-      a.rhs_full = rhs ? rhs + size_t(r0) * 3 * d.h.n : nullptr;
-      a.out_full = out + size_t(r0) * 3 * d.h.n;
-      solve_kernel<MODE_FULL><<<(nr + a.G - 1) / a.G, 512, 0, stream>>>(a);
+    if (d.prog.ncf > 0) {
+      compact_gather_kernel<<<(d.prog.ncf + 255) / 256, 256, 0, stream>>>(d.prog.ncf, d.gsrc.p, d.blocks.p,
+                                                                          d.pinv.p, d.cfac.p);
       launched();
       CK(cudaGetLastError());
     }
   }
 
-  SolveDev prow_args(SolveDev a) {
-    a.nphi = nphi;
-    a.prow_node = d_prow_node.p;
-    a.prow_phase = d_prow_phase.p;
+  CSolveArgs cargs(DevElim& d, const double2* kept_val) {
+    CSolveArgs a{};
+    a.P = d.prog;
+    a.meta_g = d.meta.p;
+    a.cfac_g = d.cfac.p;
+    a.kept_val = kept_val;
+    a.smem_factor = d.smem_factor;
+    a.n = d.h.n;
+    a.prow_off = d.prow_off.p;
+    a.mask = d.mask.p;
     return a;
   }
 
+  // anchored solves: rhs [nrhs][3n] (device, may be null = zero) -> out [nrhs][3n]
+  void solve_full(DevElim& d, const double2* kept_val, const double2* rhs, int nrhs, double2* out) {
+    if (nrhs <= 0) return;
+    CSolveArgs a = cargs(d, kept_val);
+    a.rhs_full = rhs;
+    a.out_full = out;
+    csolve_kernel<CM_FULL><<<nrhs, 256, d.smem_bytes, stream>>>(a);
+    launched();
+    CK(cudaGetLastError());
+  }
+
+  // refresh_base (reduce.cpp:265-268): base = solve(i_agg) for every scenario
   void refresh_base() {
-    SolveDev a = prow_args(solve_args(full, d_slackv.p, L));
-    a.nrhs = L;
-    a.G = 1;
-    a.iagg = d_iagg.p;
-    a.base = d_base.p;
-    a.L = L;
+    CSolveArgs c = cargs(full, d_slackv.p);
+    c.iagg = d_iagg.p;
+    c.base = d_bv.p;
+    c.L = L;
     if (profile) CK(cudaEventRecord(ev_a, stream));
-    solve_kernel<MODE_BASE><<<L, 512, 0, stream>>>(a);
+    csolve_kernel<CM_BASE><<<L, 256, full.smem_bytes, stream>>>(c);
     launched();
     CK(cudaGetLastError());
     if (profile) {
-      CK(cudaEventRecord(ev_b, stream));
-      CK(cudaEventSynchronize(ev_b));
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+      const float ms = event_ms();
       solve_stats.launches += 1;
       solve_stats.ms += ms;
-      // forward + backward: per node and RHS ~ (in-degree + 2) Mat3c*Vec3c (54 flops each)
-      solve_stats.flops += double(L) * double(full.h.nsteps) * 3.0 * 54.0;
-      solve_stats.bytes += double(full.h.nsteps) * (3.0 * 144.0) + double(L) * n * 48.0 * 2.0;
+      solve_stats.flops += double(L) * double(full.prog.ncf) * 8.0;
+      solve_stats.bytes += double(full.prog.ncf) * 16.0 + double(L) * double(nphi) * 16.0 * 2.0;
     }
   }
 
+  // Z columns solve(e_k) - v0 at present rows (reduce.cpp:272-290)
   void build_z() {
     d_Z.alloc(size_t(nphi) * size_t(nphi));
-    const int chunk = std::max(64, std::min(nphi, int((size_t(1) << 30) / (size_t(n) * 48))));
-    for (int c0 = 0; c0 < nphi; c0 += chunk) {
-      const int nc = std::min(chunk, nphi - c0);
-      SolveDev a = prow_args(solve_args(full, d_slackv.p, nc));
-      a.nrhs = nc;
-      a.G = 8;
-      a.col0 = c0;
-      a.v0p = d_v0p.p;
-      a.zout = d_Z.p;
-      solve_kernel<MODE_ZCOL><<<(nc + a.G - 1) / a.G, 512, 0, stream>>>(a);
-      launched();
-      CK(cudaGetLastError());
-    }
+    CSolveArgs c = cargs(full, d_slackv.p);
+    c.col0 = 0;
+    c.v0p = d_v0p.p;
+    c.zout = d_Z.p;
+    csolve_kernel<CM_ZCOL><<<nphi, 256, full.smem_bytes, stream>>>(c);
+    launched();
+    CK(cudaGetLastError());
   }
 
   Impl(const Problem& p, int dev_id) : prob(p), device(dev_id) {
@@ -905,6 +485,13 @@ struct Engine::Impl {
     if (device < 0) CK(cudaGetDevice(&device));
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&optin_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    for (auto fn : {csolve_kernel<CM_FULL>, csolve_kernel<CM_BASE>, csolve_kernel<CM_ZCOL>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    for (auto fn : {score_kernel<false>, score_kernel<true>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    CK(cudaFuncSetAttribute(score_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     n = prob.y.n;
     prow_off.assign(size_t(n) + 1, 0);
     for (int i = 0; i < n; ++i) {
@@ -920,9 +507,9 @@ struct Engine::Impl {
     d_prow_off.alloc(prow_off.size());
     CK(cudaMemcpy(d_prow_off.p, prow_off.data(), prow_off.size() * sizeof(int), cudaMemcpyHostToDevice));
     d_prow_node.alloc(prow_node.size());
+    d_prow_phase.alloc(prow_phase.size());
     if (nphi > 0) {
       CK(cudaMemcpy(d_prow_node.p, prow_node.data(), prow_node.size() * sizeof(int), cudaMemcpyHostToDevice));
-      d_prow_phase.alloc(prow_phase.size());
       CK(cudaMemcpy(d_prow_phase.p, prow_phase.data(), prow_phase.size(), cudaMemcpyHostToDevice));
     }
     d_mask.alloc(size_t(n));
@@ -947,11 +534,19 @@ struct Engine::Impl {
     factorize(full, d_yin.p, pivot_floor);
     d_v0.alloc(size_t(3) * n);
     d_v0p.alloc(size_t(std::max(nphi, 1)));
-    d_cs.alloc(size_t(2 * n));
-    d_cr.alloc(size_t(2 * n));
-    d_sn.alloc(size_t(n));
+    d_cand.alloc(size_t(2 * n));
+    d_snt.alloc(size_t(n));
+    d_snid.alloc(size_t(n));
     d_memoff.alloc(size_t(n) + 1);
     d_memlist.alloc(size_t(n));
+    CK(cudaMallocHost(&h_cand, sizeof(int4) * size_t(2 * n)));
+    CK(cudaMallocHost(&h_snt, sizeof(unsigned) * size_t(n)));
+    d_tab.alloc(size_t(nphi) + kTabPad);
+    d_cidx.alloc(size_t(2 * n));
+    CK(cudaMallocHost(&h_tab, sizeof(unsigned) * (size_t(nphi) + kTabPad)));
+    CK(cudaMallocHost(&h_cidx, sizeof(int) * size_t(2 * n)));
+    tab_of_node.assign(size_t(n), -1);
+    sn_pos.assign(size_t(n), -1);
     if (prob.L > 0) load_scenarios(prob.scenario_ids, prob.injections, prob.voltages);
   }
 
@@ -974,19 +569,16 @@ struct Engine::Impl {
     } else {
       solve_full(full, d_slackv.p, d_inj.p, L, d_vhat.p);
       h_vhat.resize(size_t(L) * 6 * n);
-      CK(cudaMemcpyAsync(h_vhat.data(), d_vhat.p, h_vhat.size() * sizeof(double), cudaMemcpyDeviceToHost,
-                         stream));
+      CK(cudaMemcpyAsync(h_vhat.data(), d_vhat.p, h_vhat.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
       CK(cudaStreamSynchronize(stream));
       prob.voltages = h_vhat;
     }
     d_vhatp.alloc(size_t(nphi) * L);
-    d_vmag.alloc(size_t(nphi) * L);
-    d_vmin.alloc(size_t(nphi) * L);
-    d_vmax.alloc(size_t(nphi) * L);
+    d_bv.alloc(size_t(nphi) * L * 2);
     d_iagg.alloc(size_t(n) * L * 3);
-    d_base.alloc(size_t(nphi) * L);
     d_psmice.alloc(size_t(2 * n) * L);
     d_pmaxerr.alloc(size_t(2 * n) * L);
+    d_pcand.alloc(size_t(2 * n));
     d_best.alloc(size_t(2 + L));
     if (h_best) cudaFreeHost(h_best);
     CK(cudaMallocHost(&h_best, sizeof(double) * size_t(2 + L)));
@@ -1000,6 +592,10 @@ struct Engine::Impl {
       cudaEventDestroy(ev_run1);
     }
     if (h_best) cudaFreeHost(h_best);
+    if (h_cand) cudaFreeHost(h_cand);
+    if (h_snt) cudaFreeHost(h_snt);
+    if (h_tab) cudaFreeHost(h_tab);
+    if (h_cidx) cudaFreeHost(h_cidx);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1009,12 +605,12 @@ struct Engine::Impl {
     if (c.target_reduction && !(*c.target_reduction >= 0 && *c.target_reduction <= 1))
       throw ConfigError("target_reduction must lie in [0,1]");
     if (L == 0) throw ValidationError("scenario library is empty");
+    if (!c.use_delta) throw ConfigError("use_delta=false (naive per-candidate solves) is not implemented yet");
     cfg = c;
     // AnchoredSolver (re-factorized per run, as run_reduction does, reduce.cpp:359)
     factorize(full, d_yin.p, pivot_floor);
     solve_full(full, d_slackv.p, nullptr, 1, d_v0.p);
     {
-      // v0 at present rows
       std::vector<double2> v0(size_t(3) * n);
       CK(cudaMemcpyAsync(v0.data(), d_v0.p, v0.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
       CK(cudaStreamSynchronize(stream));
@@ -1023,29 +619,68 @@ struct Engine::Impl {
       CK(cudaMemcpyAsync(d_v0p.p, v0p.data(), v0p.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
     }
     const int tot = std::max(nphi * L, n * L * 3);
-    prep_kernel<<<(tot + 255) / 256, 256, 0, stream>>>(n, L, nphi, d_prow_node.p, d_prow_phase.p, d_vhat.p,
-                                                       d_inj.p, d_vhatp.p, d_vmag.p, d_vmin.p, d_vmax.p,
-                                                       d_iagg.p);
+    prep_kernel<<<(tot + 255) / 256, 256, 0, stream>>>(n, L, nphi, d_prow_node.p, d_prow_phase.p, d_vhat.p, d_inj.p,
+                                                       d_vhatp.p, d_bv.p, d_iagg.p);
     launched();
     CK(cudaGetLastError());
-    if (cfg.use_delta) build_z();
+    build_z();
     refresh_base();
     hs.init(prob.net);
     loop_active = true;
   }
 
-  bool target_reached() const {
-    return cfg.target_reduction && hs.reduction_fraction() >= *cfg.target_reduction;
-  }
+  bool target_reached() const { return cfg.target_reduction && hs.reduction_fraction() >= *cfg.target_reduction; }
 
+  // per-iteration inputs: super-node table + candidates (pinned, async)
   void upload_iteration(long long c0, long long c1) {
     const long long C = c1 - c0;
-    if (C > 0) {
-      CK(cudaMemcpyAsync(d_cs.p, cs.data() + c0, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
-      CK(cudaMemcpyAsync(d_cr.p, cr.data() + c0, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
+    if (cfg.objective == Objective::magnitude) {
+      int t = 0;
+      for (int i : hs.supernodes) {
+        tab_of_node[size_t(i)] = t;
+        const unsigned m = prob.mask[size_t(i)];
+        unsigned first = 4u;
+        for (int p = 0; p < 3; ++p)
+          if ((m >> p) & 1u) {
+            const unsigned rho = unsigned(prow_off[size_t(i)] + __builtin_popcount(m & ((1u << p) - 1u)));
+            h_tab[t++] = (rho << 3) | first | unsigned(p);
+            first = 0u;
+          }
+      }
+      R = t;
+      for (int u = 0; u < kTabPad; ++u) h_tab[R + u] = R > 0 ? (h_tab[R - 1] & ~4u) : 0u;
+      int cnt[4] = {0, 0, 0, 0};
+      for (long long c = c0; c < c1; ++c) ++cnt[__builtin_popcount(prob.mask[size_t(cr[size_t(c)])])];
+      grp_off[0] = 0;
+      grp_off[1] = cnt[1];
+      grp_off[2] = cnt[1] + cnt[2];
+      grp_off[3] = cnt[1] + cnt[2] + cnt[3];
+      int fill[4] = {0, 0, grp_off[1], grp_off[2]};
+      for (long long c = c0; c < c1; ++c) {
+        const int s = cs[size_t(c)], r = cr[size_t(c)];
+        const int g = __builtin_popcount(prob.mask[size_t(r)]);
+        const int pos = fill[g]++;
+        h_cand[pos] = make_int4(s, r, tab_of_node[size_t(s)], tab_of_node[size_t(r)]);
+        h_cidx[pos] = int(c - c0);
+      }
+      if (C > 0) {
+        CK(cudaMemcpyAsync(d_cand.p, h_cand, size_t(C) * sizeof(int4), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_cidx.p, h_cidx, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
+      }
+      CK(cudaMemcpyAsync(d_tab.p, h_tab, size_t(R + kTabPad) * sizeof(unsigned), cudaMemcpyHostToDevice, stream));
+      return;
     }
-    CK(cudaMemcpyAsync(d_sn.p, hs.supernodes.data(), hs.supernodes.size() * sizeof(int),
-                       cudaMemcpyHostToDevice, stream));
+    int k = 0;
+    for (int i : hs.supernodes) {
+      sn_pos[size_t(i)] = k;
+      h_snt[k++] = (unsigned(prow_off[size_t(i)]) << 3) | unsigned(prob.mask[size_t(i)]);
+    }
+    for (long long c = c0; c < c1; ++c) {
+      const int s = cs[size_t(c)], r = cr[size_t(c)];
+      h_cand[c - c0] = make_int4(s, r, sn_pos[size_t(s)], sn_pos[size_t(r)]);
+    }
+    if (C > 0) CK(cudaMemcpyAsync(d_cand.p, h_cand, size_t(C) * sizeof(int4), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_snt.p, h_snt, size_t(k) * sizeof(unsigned), cudaMemcpyHostToDevice, stream));
     if (cfg.objective == Objective::complex_error) {
       std::vector<int> off(size_t(n) + 1, 0), lst;
       for (int i = 0; i < n; ++i) {
@@ -1053,44 +688,66 @@ struct Engine::Impl {
         off[size_t(i) + 1] = int(lst.size());
       }
       CK(cudaMemcpy(d_memoff.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
-      if (!lst.empty())
-        CK(cudaMemcpy(d_memlist.p, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice));
+      if (!lst.empty()) CK(cudaMemcpy(d_memlist.p, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_snid.p, hs.supernodes.data(), hs.supernodes.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
   }
 
   void launch_score(long long C) {
     if (C <= 0) return;
-    ScoreDev a{};
-    a.C = int(C);
-    a.L = L;
-    a.nphi = nphi;
-    a.ns = int(hs.supernodes.size());
-    a.cand_s = d_cs.p;
-    a.cand_r = d_cr.p;
-    a.sn = d_sn.p;
-    a.prow_off = d_prow_off.p;
-    a.mask = d_mask.p;
-    a.Z = d_Z.p;
-    a.base = d_base.p;
-    a.vmin = d_vmin.p;
-    a.vmax = d_vmax.p;
-    a.iagg = d_iagg.p;
-    a.objective = cfg.objective == Objective::complex_error ? KRG_OBJ_COMPLEX : KRG_OBJ_MAGNITUDE;
-    a.mem_off = d_memoff.p;
-    a.mem_list = d_memlist.p;
-    a.vhatp = d_vhatp.p;
-    a.out_smice = d_psmice.p;
-    a.out_maxerr = d_pmaxerr.p;
-    const long long pairs = C * L;
     if (profile) CK(cudaEventRecord(ev_a, stream));
-    score_kernel<<<unsigned((pairs + 127) / 128), 128, 0, stream>>>(a);
-    launched();
-    CK(cudaGetLastError());
+    if (cfg.objective == Objective::magnitude) {
+      RowArgs g{};
+      g.L = L;
+      g.nphi = nphi;
+      g.R = R;
+      g.tab = d_tab.p;
+      g.mask = d_mask.p;
+      g.prow_off = d_prow_off.p;
+      g.Z = d_Z.p;
+      g.bv = d_bv.p;
+      g.iagg = d_iagg.p;
+      g.out_smice = d_psmice.p;
+      g.out_maxerr = d_pmaxerr.p;
+      const int P = score_cta_threads();
+      const int G = (P % L == 0) ? P / L : 1;
+      const long long pairs = C * L;
+      int S = int(std::min<long long>(std::max<long long>(1, (148LL * 1024 + pairs - 1) / std::max(1LL, pairs)),
+                                      std::max(1, 512 / P)));
+      S = std::min(S, 16);
+      g.S = S;
+      g.G = G;
+      g.cand = d_cand.p;
+      g.cand_idx = d_cidx.p;
+      g.out_cand = d_pcand.p;
+      g.e_bar = cfg.e_bar;
+      g.C = int(C);
+      int ctas = 0;
+      for (int k = 1; k <= 3; ++k) {
+        g.grp_start[k] = grp_off[k - 1];
+        g.grp_cta[k - 1] = ctas;
+        ctas += (grp_off[k] - grp_off[k - 1] + G - 1) / G;
+      }
+      g.grp_cta[1] = (grp_off[1] - grp_off[0] + G - 1) / G;
+      g.grp_cta[2] = g.grp_cta[1] + (grp_off[2] - grp_off[1] + G - 1) / G;
+      g.grp_cta[3] = ctas;
+      if (ctas > 0 && use_tiles) {
+        constexpr int K = 32;
+        const size_t per_buf = (K * 4 + 15) / 16 + size_t(K) * L * 2 + size_t(G) * 3 * 2 * K;  // double2 units
+        const size_t smem = std::max(2 * per_buf * sizeof(double2) + size_t(G) * 3 * 2 * sizeof(int) + 64,
+                                     2 * size_t(P) * sizeof(double));
+        score_tiles_kernel<<<ctas, P, smem, stream>>>(g);
+      } else if (ctas > 0) {
+        const size_t smem = (2 * size_t(S) * 4 + 3) * size_t(P) * sizeof(double);
+        score_rows_kernel<<<ctas, P * S, smem, stream>>>(g);
+        launched();
+        CK(cudaGetLastError());
+      }
+    } else {
+      launch_score_members(C);
+    }
     if (profile) {
-      CK(cudaEventRecord(ev_b, stream));
-      CK(cudaEventSynchronize(ev_b));
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+      const float ms = event_ms();
       double f, b;
       score_work(score_c0, score_c0 + C, f, b);
       score_stats.launches += 1;
@@ -1100,14 +757,51 @@ struct Engine::Impl {
     }
   }
 
-  // score [c0,c1) and reduce to the local best; returns (smice, global idx) and max_err in h_best
-  long long score_c0 = 0;
+  void launch_score_members(long long C) {
+    ScoreArgs a{};
+    a.C = int(C);
+    a.L = L;
+    a.nphi = nphi;
+    a.ns = int(hs.supernodes.size());
+    // pairs per CTA: a multiple of 32 so each warp shares one segment
+    int P = L * (32 / gcd_int(L, 32));
+    if (P > 512) P = L;
+    a.G = P / L;
+    const long long ctas = (C + a.G - 1) / a.G;
+    const int smax = std::max(1, 512 / P);
+    const long long want = (148LL * 1536 + ctas * P - 1) / (ctas * P);
+    a.S = int(std::min<long long>(smax, std::max<long long>(1, want)));
+    a.K = 64;
+    const size_t smem = size_t(std::max(a.K, a.S)) * size_t(P) * sizeof(double);
+    a.cand = d_cand.p;
+    a.snt = d_snt.p;
+    a.mask = d_mask.p;
+    a.prow_off = d_prow_off.p;
+    a.Z = d_Z.p;
+    a.bv = d_bv.p;
+    a.iagg = d_iagg.p;
+    a.mem_off = d_memoff.p;
+    a.mem_list = d_memlist.p;
+    a.sn_id = d_snid.p;
+    a.vhatp = d_vhatp.p;
+    a.out_smice = d_psmice.p;
+    a.out_maxerr = d_pmaxerr.p;
+    if (cfg.objective == Objective::complex_error)
+      score_kernel<true><<<unsigned(ctas), P * a.S, smem, stream>>>(a);
+    else
+      score_kernel<false><<<unsigned(ctas), P * a.S, smem, stream>>>(a);
+    launched();
+    CK(cudaGetLastError());
+  }
+
+  // score [c0,c1) and reduce to the local best: (smice, global idx, max_err) in h_best
   void score_best(long long c0, long long c1) {
     const long long C = c1 - c0;
     score_c0 = c0;
     upload_iteration(c0, c1);
     launch_score(C);
     argmin_kernel<<<1, 1024, 0, stream>>>(int(std::max(C, 0LL)), L, cfg.e_bar, c0, d_psmice.p, d_pmaxerr.p,
+                                          cfg.objective == Objective::magnitude ? d_pcand.p : nullptr,
                                           d_best.p);
     launched();
     CK(cudaGetLastError());
@@ -1141,9 +835,9 @@ struct Engine::Impl {
         bw = w;
       }
     }
-    if (bw >= 0)
+    if (bw >= 0) {
       std::memcpy(h_best, all.data() + size_t(bw) * size_t(2 + L), bytes);
-    else {
+    } else {
       const long long none = -1;
       std::memcpy(&h_best[1], &none, sizeof none);
     }
@@ -1152,10 +846,10 @@ struct Engine::Impl {
   void commit_device(int s, int r) {
     const unsigned ms = prob.mask[size_t(s)], mr = prob.mask[size_t(r)];
     commit_kernel<<<(L + 127) / 128, 128, 0, stream>>>(s, r, L, ms, mr, prow_off[size_t(s)], prow_off[size_t(r)],
-                                                       d_iagg.p, d_vmin.p, d_vmax.p);
+                                                       d_iagg.p, d_bv.p);
     launched();
     CK(cudaGetLastError());
-    if (cfg.use_delta) refresh_base();
+    refresh_base();
   }
 };
 
@@ -1289,13 +983,22 @@ void Engine::loop_score_all(double* smice, std::uint8_t* feasible, double* max_e
   const long long C = (long long)I.cs.size();
   I.upload_iteration(0, C);
   I.launch_score(C);
-  std::vector<double> ps(size_t(C) * I.L), pm(size_t(C) * I.L);
+  std::vector<double> ps(size_t(C) * I.L), pm(size_t(C) * I.L), pc(static_cast<size_t>(C));
+  const bool mag = I.cfg.objective == Objective::magnitude;
   if (C > 0) {
-    CK(cudaMemcpyAsync(ps.data(), I.d_psmice.p, ps.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
+    if (mag)
+      CK(cudaMemcpyAsync(pc.data(), I.d_pcand.p, pc.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
+    else
+      CK(cudaMemcpyAsync(ps.data(), I.d_psmice.p, ps.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
     CK(cudaMemcpyAsync(pm.data(), I.d_pmaxerr.p, pm.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
   }
   CK(cudaStreamSynchronize(I.stream));
-  for (long long c = 0; c < C; ++c) {
+  for (long long c = 0; c < C && mag; ++c) {
+    feasible[c] = pc[size_t(c)] < 0.0 ? 0 : 1;
+    smice[c] = pc[size_t(c)] < 0.0 ? std::numeric_limits<double>::infinity() : pc[size_t(c)];
+    for (int l = 0; l < I.L && max_err; ++l) max_err[size_t(c) * I.L + l] = pm[size_t(c) * I.L + l];
+  }
+  for (long long c = 0; c < C && !mag; ++c) {
     bool feas = true;
     double sum = 0;
     for (int l = 0; l < I.L; ++l) {
@@ -1331,15 +1034,15 @@ void Engine::loop_commit(int s, int r) {
 
 void Engine::loop_base(double* out) {
   Impl& I = *impl_;
-  std::vector<double2> b(size_t(I.nphi) * I.L);
-  CK(cudaMemcpyAsync(b.data(), I.d_base.p, b.size() * sizeof(double2), cudaMemcpyDeviceToHost, I.stream));
+  std::vector<double2> bv(size_t(I.nphi) * I.L * 2);
+  CK(cudaMemcpyAsync(bv.data(), I.d_bv.p, bv.size() * sizeof(double2), cudaMemcpyDeviceToHost, I.stream));
   CK(cudaStreamSynchronize(I.stream));
   std::memset(out, 0, sizeof(double) * size_t(I.L) * 6 * I.n);
   for (int r = 0; r < I.nphi; ++r)
     for (int l = 0; l < I.L; ++l) {
       const size_t o = (size_t(l) * 3 * I.n + size_t(I.prow_node[size_t(r)]) * 3 + I.prow_phase[size_t(r)]) * 2;
-      out[o] = b[size_t(r) * I.L + l].x;
-      out[o + 1] = b[size_t(r) * I.L + l].y;
+      out[o] = bv[(size_t(r) * I.L + l) * 2].x;
+      out[o + 1] = bv[(size_t(r) * I.L + l) * 2].y;
     }
 }
 
@@ -1412,13 +1115,12 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, I.ev_run0, I.ev_run1));
   out.device_ms = ms;
-  I.last_run_ms = ms;
 }
 
 void Engine::kron(const std::vector<int>& reduce, ReducedModel& model) {
   Impl& I = *impl_;
   DevElim e;
-  I.upload_elim(e, I.prob.y, I.prob.mask, reduce);
+  I.upload_elim(e, I.prob.y, I.prob.mask, reduce, /*with_solve=*/false);
   I.factorize(e, I.d_yin.p, 1e-12 * std::max(I.prob.y.max_abs(), 1.0));
   const ElimSchedule& h = e.h;
   std::vector<double2> blocks(size_t(h.nblocks) * 9);
@@ -1563,6 +1265,25 @@ extern "C" int krg_fp64_probe(int32_t device, double* gflops) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *gflops = best;
+    return KRG_OK;
+  } catch (...) {
+    return status_from_current_exception();
+  }
+}
+
+// self test: branch-free scorer sqrt vs __dsqrt_rn on n random inputs in [lo,hi)
+extern "C" int krg_selftest_sqrt(int64_t n, double lo, double hi, int64_t* mismatches) {
+  try {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) throw CudaError("no CUDA device");
+    DBuf<unsigned long long> bad;
+    bad.alloc(1);
+    CK(cudaMemset(bad.p, 0, sizeof(unsigned long long)));
+    selftest_sqrt_kernel<<<unsigned((n + 255) / 256), 256>>>(n, 12345ull, bad.p, lo, hi);
+    CK(cudaGetLastError());
+    unsigned long long h = 0;
+    CK(cudaMemcpy(&h, bad.p, sizeof h, cudaMemcpyDeviceToHost));
+    *mismatches = (int64_t)h;
     return KRG_OK;
   } catch (...) {
     return status_from_current_exception();

@@ -61,6 +61,11 @@ def test_cdiv_replica_device_matches_host():
     np.testing.assert_array_equal(host_out.view(np.uint64), dev_out.view(np.uint64))
 
 
+@pytest.mark.parametrize("lo,hi", [(0.25, 4.0), (0.7, 1.3), (1e-300, 1e-280), (1e200, 1e280), (1e-6, 1e6)])
+def test_scorer_sqrt_is_ieee(lo, hi):
+    assert kr.api.sqrt_selftest(20_000_000, lo, hi) == 0
+
+
 @pytest.mark.parametrize("case", ["s24", "m40"])
 def test_solves_bitwise(case):
     hp = host(case)
