@@ -174,6 +174,8 @@ int krg_loop_commit(krg_ctx* ctx, int32_t s, int32_t r);
 int krg_zcols(krg_ctx* ctx, double* out, int64_t cap);
 /* Per-iteration base voltages (refresh_base, reduce.cpp:265-268): [L][3n][2]. */
 int krg_loop_base(krg_ctx* ctx, double* out);
+/* Benchmark hook: mean time of `reps` base refreshes and block-0 phase clocks. */
+int krg_debug_base_refresh(krg_ctx* ctx, int32_t reps, double* ms, long long* clocks);
 
 /* kron_reduce (kron.cpp:34-46) of the context's Y onto keep = complement of
  * `reduce`; result read back with krg_result_* accessors (model part only). */

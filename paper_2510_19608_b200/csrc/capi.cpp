@@ -611,6 +611,13 @@ int krg_solve(krg_ctx* ctx, const double* inj, int32_t nrhs, double* out) {
   KRG_CATCH
 }
 
+int krg_debug_base_refresh(krg_ctx* ctx, int32_t reps, double* ms, long long* clocks) {
+  KRG_TRY
+  ctx->eng->debug_base_refresh(reps, ms, clocks);
+  return KRG_OK;
+  KRG_CATCH
+}
+
 int krg_loop_begin(krg_ctx* ctx, const krg_config* c) {
   KRG_TRY
   ctx->eng->loop_begin(cfg_from_c(c));

@@ -119,9 +119,16 @@ struct DevElim {
   DBuf<int> meta;
   DBuf<long long> gsrc;
   DBuf<double2> cfac;
-  DBuf<int> prow_off;
+  DBuf<int> prow_off, prow_node;
+  DBuf<std::uint8_t> prow_phase;
   std::vector<int> xoff;
   int smem_bytes = 0, smem_factor = 0;
+  int wwarps = 0, wsm_factor = 0, wsmem_bytes = 0;
+  int ncf_all = 0;  // gathered coefficients (program + padding entries)
+  // lane-slot base-refresh program (base_refresh_kernel)
+  BaseArgs bprog{};
+  DBuf<int> bmeta;
+  int bW = 0, bsmem = 0;
   const int* P(int which) const { return ints.p + off[size_t(which)]; }
 };
 
@@ -147,7 +154,7 @@ struct Engine::Impl {
   DBuf<double2> d_yin;        // assembled Y blocks (input, resident)
   double pivot_floor = 0;
   DevElim full;               // anchored factorization of Y
-  DBuf<double2> d_inj, d_vhat, d_v0, d_v0p, d_vhatp, d_iagg, d_bv, d_Z, d_slackv;
+  DBuf<double2> d_inj, d_vhat, d_v0, d_v0p, d_vhatp, d_iagg, d_iaggp, d_bv, d_Z, d_slackv;
   std::vector<double> h_vhat;  // [L][3n][2]
   // per-iteration inputs (pinned staging)
   DBuf<int4> d_cand;
@@ -260,14 +267,25 @@ struct Engine::Impl {
     if (with_solve) build_compact(d);
   }
 
-  // Host: present-phase layout of the factor and the packed level program.
+  // Host: present-phase layout of the factor and the packed level program
+  // (records in level order, see kernels_csolve.cuh).
   void build_compact(DevElim& d) {
     const ElimSchedule& h = d.h;
     const int nn = h.n;
     d.xoff.assign(size_t(nn) + 1, 0);
     for (int i = 0; i < nn; ++i) d.xoff[size_t(i) + 1] = d.xoff[size_t(i)] + __builtin_popcount(h.mask[size_t(i)]);
-    std::vector<int> st_x, st_m, st_mask, st_node, st_pinv, in_off{0}, in_x, in_m, in_blk, cp_off{0}, cp_x, cp_m,
-        cp_blk, kept_x, kept_m, kept_i;
+    const int nph = d.xoff[size_t(nn)];
+    std::vector<int> pnode(size_t(std::max(nph, 1)), 0);
+    std::vector<std::uint8_t> pphase(size_t(std::max(nph, 1)), 0);
+    for (int i = 0; i < nn; ++i) {
+      int t = d.xoff[size_t(i)];
+      for (int p = 0; p < 3; ++p)
+        if ((h.mask[size_t(i)] >> p) & 1) {
+          pnode[size_t(t)] = i;
+          pphase[size_t(t)] = std::uint8_t(p);
+          ++t;
+        }
+    }
     std::vector<long long> g;
     auto present = [&](int node, int* idx) {
       int k = 0;
@@ -284,83 +302,251 @@ struct Engine::Impl {
           g.push_back(base9 < 0 ? -1 : (((base9 + ri[i] * 3 + ci[j]) << 1) | (is_pinv ? 1 : 0)));
       return off;
     };
+    auto xm = [&](int node) {
+      const int m = __builtin_popcount(h.mask[size_t(node)]);
+      if (d.xoff[size_t(node)] >= (1 << 24)) throw Error("solution vector too large for the packed program");
+      return d.xoff[size_t(node)] | (m << 24);
+    };
+    // per-step factor offsets
+    std::vector<int> pinv_off(size_t(h.nsteps)), fin_first(size_t(h.nsteps)), bcp_first(size_t(h.nsteps));
+    std::vector<int> fin_x, fin_b, bcp_x, bcp_b;
     for (int st = 0; st < h.nsteps; ++st) {
       const int k = h.step_node[size_t(st)];
-      st_x.push_back(d.xoff[size_t(k)]);
-      st_m.push_back(__builtin_popcount(h.mask[size_t(k)]));
-      st_mask.push_back(h.mask[size_t(k)]);
-      st_node.push_back(k);
-      st_pinv.push_back(gather_block((long long)st * 9, true, k, k));
+      pinv_off[size_t(st)] = gather_block((long long)st * 9, true, k, k);
+      fin_first[size_t(st)] = int(fin_x.size());
       for (int e = h.in_off[size_t(st)]; e < h.in_off[size_t(st) + 1]; ++e) {
         const int j = h.in_node[size_t(e)], b = h.in_blk[size_t(e)];
-        in_x.push_back(d.xoff[size_t(j)]);
-        in_m.push_back(__builtin_popcount(h.mask[size_t(j)]));
-        in_blk.push_back(gather_block(b < 0 ? -1 : (long long)b * 9, false, k, j));
+        fin_x.push_back(xm(j));
+        fin_b.push_back(gather_block(b < 0 ? -1 : (long long)b * 9, false, k, j));
       }
-      in_off.push_back(int(in_x.size()));
+      bcp_first[size_t(st)] = int(bcp_x.size());
       for (int e = h.cpl_off[size_t(st)]; e < h.cpl_off[size_t(st) + 1]; ++e) {
         const int j = h.cpl_node[size_t(e)], b = h.cpl_to[size_t(e)];
-        cp_x.push_back(d.xoff[size_t(j)]);
-        cp_m.push_back(__builtin_popcount(h.mask[size_t(j)]));
-        cp_blk.push_back(gather_block(b < 0 ? -1 : (long long)b * 9, false, k, j));
+        bcp_x.push_back(xm(j));
+        bcp_b.push_back(gather_block(b < 0 ? -1 : (long long)b * 9, false, k, j));
       }
-      cp_off.push_back(int(cp_x.size()));
-    }
-    for (size_t kk = 0; kk < h.kept.size(); ++kk) {
-      kept_x.push_back(d.xoff[size_t(h.kept[kk])]);
-      kept_m.push_back(__builtin_popcount(h.mask[size_t(h.kept[kk])]));
-      kept_i.push_back(int(kk));
     }
     std::vector<int> meta;
-    auto put = [&](const std::vector<int>& v) {
-      const int o = int(meta.size());
-      meta.insert(meta.end(), v.begin(), v.end());
-      return o;
+    auto align4 = [&]() {
+      while (meta.size() % 4) meta.push_back(0);
     };
     CProg P{};
-    P.st_x = put(st_x);
-    P.st_m = put(st_m);
-    P.st_mask = put(st_mask);
-    P.st_node = put(st_node);
-    P.st_pinv = put(st_pinv);
-    P.in_off = put(in_off);
-    P.in_x = put(in_x);
-    P.in_m = put(in_m);
-    P.in_blk = put(in_blk);
-    P.cp_off = put(cp_off);
-    P.cp_x = put(cp_x);
-    P.cp_m = put(cp_m);
-    P.cp_blk = put(cp_blk);
-    P.fw_off = put(h.fw_off);
-    P.fw = put(h.fw_steps);
-    P.bw_off = put(h.bw_off);
-    P.bw = put(h.bw_steps);
-    P.kept_x = put(kept_x);
-    P.kept_m = put(kept_m);
-    P.kept_i = put(kept_i);
+    // forward records (level order) + their pull entries (contiguous per record)
+    align4();
+    P.frec = int(meta.size());
+    std::vector<int> fent;
+    for (int i = 0; i < h.nsteps && h.nsteps > 0; ++i) {
+      const int st = h.fw_steps[size_t(i)];
+      const int k = h.step_node[size_t(st)];
+      const int ne = h.in_off[size_t(st) + 1] - h.in_off[size_t(st)];
+      if (ne > 255) throw Error("elimination step has more than 255 pulls");
+      bool scalar = __builtin_popcount(h.mask[size_t(k)]) == 1;
+      for (int e = 0; e < ne; ++e) scalar = scalar && (fin_x[size_t(fin_first[size_t(st)] + e)] >> 24) == 1;
+      meta.push_back(xm(k) | (int(h.mask[size_t(k)]) << 26) | (scalar ? (1 << 29) : 0));
+      meta.push_back(k);
+      meta.push_back(pinv_off[size_t(st)]);
+      meta.push_back(int(fent.size() / 2) | (ne << 24));
+      for (int e = 0; e < ne; ++e) {
+        fent.push_back(fin_x[size_t(fin_first[size_t(st)] + e)]);
+        fent.push_back(fin_b[size_t(fin_first[size_t(st)] + e)]);
+      }
+    }
+    align4();
+    P.fent = int(meta.size());
+    meta.insert(meta.end(), fent.begin(), fent.end());
+    align4();
+    P.brec = int(meta.size());
+    std::vector<int> bent;
+    for (int i = 0; i < h.nsteps && h.nsteps > 0; ++i) {
+      const int st = h.bw_steps[size_t(i)];
+      const int k = h.step_node[size_t(st)];
+      const int ne = h.cpl_off[size_t(st) + 1] - h.cpl_off[size_t(st)];
+      if (ne > 255) throw Error("elimination step has more than 255 couplings");
+      bool scalar = __builtin_popcount(h.mask[size_t(k)]) == 1;
+      for (int e = 0; e < ne; ++e) scalar = scalar && (bcp_x[size_t(bcp_first[size_t(st)] + e)] >> 24) == 1;
+      meta.push_back(xm(k) | (scalar ? (1 << 29) : 0));
+      meta.push_back(k);
+      meta.push_back(pinv_off[size_t(st)]);
+      meta.push_back(int(bent.size() / 2) | (ne << 24));
+      for (int e = 0; e < ne; ++e) {
+        bent.push_back(bcp_x[size_t(bcp_first[size_t(st)] + e)]);
+        bent.push_back(bcp_b[size_t(bcp_first[size_t(st)] + e)]);
+      }
+    }
+    align4();
+    P.bent = int(meta.size());
+    meta.insert(meta.end(), bent.begin(), bent.end());
+    P.fw_off = int(meta.size());
+    if (h.nsteps > 0) meta.insert(meta.end(), h.fw_off.begin(), h.fw_off.end());
+    P.bw_off = int(meta.size());
+    if (h.nsteps > 0) meta.insert(meta.end(), h.bw_off.begin(), h.bw_off.end());
+    P.kept = int(meta.size());
+    for (size_t kk = 0; kk < h.kept.size(); ++kk) {
+      meta.push_back(xm(h.kept[kk]));
+      meta.push_back(int(kk));
+    }
+    align4();
     P.nsteps = h.nsteps;
     P.nfw = h.nsteps ? h.nfw : 0;
     P.nbw = h.nsteps ? h.nbw : 0;
     P.nkept = int(h.kept.size());
     P.nmeta = int(meta.size());
     P.ncf = int(g.size());
-    P.nphi = d.xoff[size_t(nn)];
+    P.nphi = nph;
     d.prog = P;
+    {
+      // lane-slot program: per level round 32 records, scalar one-entry steps inline
+      std::vector<int> bm, fe2, be2;
+      const int zero_cf = int(g.size());
+      g.push_back(-1);  // one exact-zero coefficient for pull-free steps
+      auto slots = [&](const std::vector<int>& off, const std::vector<int>& steps, bool fwd, int& nrounds,
+                       std::vector<int>& recs, std::vector<int>& ext, std::vector<int>& ents) {
+        nrounds = 0;
+        const int nl = h.nsteps ? int(off.size()) - 1 : 0;
+        auto empty = [&]() {
+          recs.insert(recs.end(), {-1, 0, 0, 0});
+          ext.insert(ext.end(), {0, 0, 0, 0});
+        };
+        for (int lv = 0; lv < nl; ++lv) {
+          const int c0 = off[size_t(lv)], cnt = off[size_t(lv) + 1] - c0;
+          for (int r0 = 0; r0 < cnt; r0 += 32, ++nrounds)
+            for (int ln = 0; ln < 32; ++ln) {
+              if (r0 + ln >= cnt) {
+                empty();
+                continue;
+              }
+              const int st = steps[size_t(c0 + r0 + ln)];
+              const int k = h.step_node[size_t(st)];
+              const int mk = __builtin_popcount(h.mask[size_t(k)]);
+              const int first = fwd ? fin_first[size_t(st)] : bcp_first[size_t(st)];
+              const int ne = fwd ? h.in_off[size_t(st) + 1] - h.in_off[size_t(st)]
+                                 : h.cpl_off[size_t(st) + 1] - h.cpl_off[size_t(st)];
+              const std::vector<int>& ex = fwd ? fin_x : bcp_x;
+              const std::vector<int>& eb = fwd ? fin_b : bcp_b;
+              bool scalar = mk == 1;
+              for (int e = 0; e < ne; ++e) scalar = scalar && (ex[size_t(first + e)] >> 24) == 1;
+              if (size_t(d.xoff[size_t(nn)]) * 16 >= (1u << 31) || size_t(g.size()) * 16 >= (1u << 31))
+                throw Error("base program offsets overflow");
+              if (scalar) {
+                // first pull inline; a pull-free step gets an exact-zero pull
+                // (b - (0 + 0*x) == b bit for bit), so every scalar step runs
+                // the same instruction sequence
+                const int xj = ne == 0 ? d.xoff[size_t(k)] : (ex[size_t(first)] & 0xffffff);
+                const int bo = ne == 0 ? zero_cf : eb[size_t(first)];
+                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, xj * 16, bo * 16});
+                ext.insert(ext.end(), {0, mk, int(ents.size() / 2), std::max(ne - 1, 0)});
+                for (int e = 1; e < ne; ++e) {
+                  ents.push_back(ex[size_t(first + e)]);
+                  ents.push_back(eb[size_t(first + e)]);
+                }
+              } else {
+                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, 0, 0});
+                ext.insert(ext.end(), {1, mk, int(ents.size() / 2), ne});
+                for (int e = 0; e < ne; ++e) {
+                  ents.push_back(ex[size_t(first + e)]);
+                  ents.push_back(eb[size_t(first + e)]);
+                }
+              }
+            }
+        }
+        for (int ln = 0; ln < 32; ++ln) empty();  // padding round for the unconditional prefetch
+      };
+      std::vector<int> frecs, brecs, fext, bext;
+      int nfr = 0, nbr = 0;
+      slots(h.fw_off, h.fw_steps, true, nfr, frecs, fext, fe2);
+      slots(h.bw_off, h.bw_steps, false, nbr, brecs, bext, be2);
+      BaseArgs& B = d.bprog;
+      auto put4 = [&](const std::vector<int>& v) {
+        while (bm.size() % 4) bm.push_back(0);
+        const int o = int(bm.size());
+        bm.insert(bm.end(), v.begin(), v.end());
+        return o;
+      };
+      B.fslot = put4(frecs);
+      B.bslot = put4(brecs);
+      B.fext = put4(fext);
+      B.bext = put4(bext);
+      B.fent = put4(fe2);
+      B.bent = put4(be2);
+      std::vector<int> kp;
+      for (size_t kk = 0; kk < h.kept.size(); ++kk) {
+        kp.push_back(xm(h.kept[kk]));
+        kp.push_back(int(kk));
+      }
+      B.kept = put4(kp);
+      while (bm.size() % 4) bm.push_back(0);
+      B.nfr = nfr;
+      B.nbr = nbr;
+      B.nkept = int(h.kept.size());
+      B.nmeta = int(bm.size());
+      B.ncf = int(g.size());
+      B.nphi = nph;
+      d.bmeta.alloc(bm.size());
+      CK(cudaMemcpyAsync(d.bmeta.p, bm.data(), bm.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+      const size_t fixed = size_t(B.ncf) * 16 + size_t(B.nmeta) * 4;
+      d.bW = 0;
+      for (int w = 8; w >= 1; --w)
+        if (fixed + size_t(w) * size_t(nph) * 16 <= size_t(optin_smem) - 64) {
+          d.bW = w;
+          break;
+        }
+      d.bsmem = int(fixed + size_t(std::max(d.bW, 1)) * size_t(nph) * 16);
+    }
     d.meta.alloc(meta.size());
     if (!meta.empty())
       CK(cudaMemcpyAsync(d.meta.p, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+    d.ncf_all = int(g.size());
     d.gsrc.alloc(g.size());
     if (!g.empty())
       CK(cudaMemcpyAsync(d.gsrc.p, g.data(), g.size() * sizeof(long long), cudaMemcpyHostToDevice, stream));
     d.cfac.alloc(g.size());
     d.prow_off.alloc(d.xoff.size());
     CK(cudaMemcpyAsync(d.prow_off.p, d.xoff.data(), d.xoff.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+    d.prow_node.alloc(pnode.size());
+    CK(cudaMemcpyAsync(d.prow_node.p, pnode.data(), pnode.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+    d.prow_phase.alloc(pphase.size());
+    CK(cudaMemcpyAsync(d.prow_phase.p, pphase.data(), pphase.size(), cudaMemcpyHostToDevice, stream));
+    // cfac starts at a 16-byte boundary after x; the int program after cfac
     const size_t xb = size_t(P.nphi) * sizeof(double2);
     const size_t all = xb + size_t(P.ncf) * sizeof(double2) + size_t(P.nmeta) * sizeof(int);
     if (xb > size_t(optin_smem)) throw Error("solution vector does not fit in shared memory");
     d.smem_factor = all <= size_t(optin_smem) ? 1 : 0;
     d.smem_bytes = int(d.smem_factor ? all : xb);
+    // warp-per-rhs layout: staged factor + W solution vectors
+    const size_t fac = size_t(P.ncf) * sizeof(double2) + size_t(P.nmeta) * sizeof(int);
+    d.wsm_factor = 0;
+    d.wwarps = 0;
+    for (int w = 8; w >= 1; w /= 2)
+      if (fac + size_t(w) * xb <= size_t(optin_smem)) {
+        d.wsm_factor = 1;
+        d.wwarps = w;
+        break;
+      }
+    if (!d.wsm_factor)
+      for (int w = 8; w >= 1; w /= 2)
+        if (size_t(w) * xb <= size_t(optin_smem)) {
+          d.wwarps = w;
+          break;
+        }
+    d.wsmem_bytes = int((d.wsm_factor ? fac : 0) + size_t(std::max(d.wwarps, 1)) * xb);
     CK(cudaStreamSynchronize(stream));
+  }
+
+  template <int MODE>
+  void launch_csolve(DevElim& d, const CSolveArgs& c, int nrhs) {
+    if (nrhs <= 0) return;
+    if (d.wwarps > 0) {
+      const int W = d.wwarps;
+      const unsigned grid = unsigned((nrhs + W - 1) / W);
+      if (d.wsm_factor)
+        csolve_warp_kernel<MODE, true><<<grid, 32 * W, d.wsmem_bytes, stream>>>(c, nrhs);
+      else
+        csolve_warp_kernel<MODE, false><<<grid, 32 * W, d.wsmem_bytes, stream>>>(c, nrhs);
+    } else {
+      csolve_kernel<MODE><<<nrhs, 256, d.smem_bytes, stream>>>(c);
+    }
+    launched();
+    CK(cudaGetLastError());
   }
 
   // K1f on the device: blocks <- input, fill <- 0, then the level executor,
@@ -415,9 +601,9 @@ struct Engine::Impl {
                             std::to_string(h.nsteps) + " eliminations left)",
                         piv, node);
     }
-    if (d.prog.ncf > 0) {
-      compact_gather_kernel<<<(d.prog.ncf + 255) / 256, 256, 0, stream>>>(d.prog.ncf, d.gsrc.p, d.blocks.p,
-                                                                          d.pinv.p, d.cfac.p);
+    if (d.ncf_all > 0) {
+      compact_gather_kernel<<<(d.ncf_all + 255) / 256, 256, 0, stream>>>(d.ncf_all, d.gsrc.p, d.blocks.p,
+                                                                         d.pinv.p, d.cfac.p);
       launched();
       CK(cudaGetLastError());
     }
@@ -433,6 +619,8 @@ struct Engine::Impl {
     a.n = d.h.n;
     a.prow_off = d.prow_off.p;
     a.mask = d.mask.p;
+    a.prow_node = d.prow_node.p;
+    a.prow_phase = d.prow_phase.p;
     return a;
   }
 
@@ -442,21 +630,42 @@ struct Engine::Impl {
     CSolveArgs a = cargs(d, kept_val);
     a.rhs_full = rhs;
     a.out_full = out;
-    csolve_kernel<CM_FULL><<<nrhs, 256, d.smem_bytes, stream>>>(a);
-    launched();
-    CK(cudaGetLastError());
+    launch_csolve<CM_FULL>(d, a, nrhs);
   }
 
   // refresh_base (reduce.cpp:265-268): base = solve(i_agg) for every scenario
+  long long* dbg_clock = nullptr;
   void refresh_base() {
+    if (full.bW > 0) {
+      BaseArgs b = full.bprog;
+      b.L = L;
+      b.W = full.bW;
+      b.cfac = full.cfac.p;
+      b.meta = full.bmeta.p;
+      b.iaggp = d_iaggp.p;
+      b.kept_val = d_slackv.p;
+      b.bv = d_bv.p;
+      b.dbg = dbg_clock;
+      if (profile) CK(cudaEventRecord(ev_a, stream));
+      base_refresh_kernel<<<(L + b.W - 1) / b.W, 32 * b.W, full.bsmem, stream>>>(b);
+      launched();
+      CK(cudaGetLastError());
+      if (profile) {
+        const float ms = event_ms();
+        solve_stats.launches += 1;
+        solve_stats.ms += ms;
+        solve_stats.flops += double(L) * double(full.prog.ncf) * 8.0;
+        solve_stats.bytes += double(full.prog.ncf) * 16.0 + double(L) * double(nphi) * 16.0 * 2.0;
+      }
+      return;
+    }
     CSolveArgs c = cargs(full, d_slackv.p);
+    c.dbg = dbg_clock;
     c.iagg = d_iagg.p;
     c.base = d_bv.p;
     c.L = L;
     if (profile) CK(cudaEventRecord(ev_a, stream));
-    csolve_kernel<CM_BASE><<<L, 256, full.smem_bytes, stream>>>(c);
-    launched();
-    CK(cudaGetLastError());
+    launch_csolve<CM_BASE>(full, c, L);
     if (profile) {
       const float ms = event_ms();
       solve_stats.launches += 1;
@@ -473,9 +682,7 @@ struct Engine::Impl {
     c.col0 = 0;
     c.v0p = d_v0p.p;
     c.zout = d_Z.p;
-    csolve_kernel<CM_ZCOL><<<nphi, 256, full.smem_bytes, stream>>>(c);
-    launched();
-    CK(cudaGetLastError());
+    launch_csolve<CM_ZCOL>(full, c, nphi);
   }
 
   Impl(const Problem& p, int dev_id) : prob(p), device(dev_id) {
@@ -488,9 +695,14 @@ struct Engine::Impl {
     CK(cudaDeviceGetAttribute(&optin_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     for (auto fn : {csolve_kernel<CM_FULL>, csolve_kernel<CM_BASE>, csolve_kernel<CM_ZCOL>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    for (auto fn : {csolve_warp_kernel<CM_FULL, true>, csolve_warp_kernel<CM_BASE, true>,
+                    csolve_warp_kernel<CM_ZCOL, true>, csolve_warp_kernel<CM_FULL, false>,
+                    csolve_warp_kernel<CM_BASE, false>, csolve_warp_kernel<CM_ZCOL, false>})
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     for (auto fn : {score_kernel<false>, score_kernel<true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    CK(cudaFuncSetAttribute(base_refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     n = prob.y.n;
     prow_off.assign(size_t(n) + 1, 0);
@@ -576,6 +788,7 @@ struct Engine::Impl {
     d_vhatp.alloc(size_t(nphi) * L);
     d_bv.alloc(size_t(nphi) * L * 2);
     d_iagg.alloc(size_t(n) * L * 3);
+    d_iaggp.alloc(size_t(L) * std::max(nphi, 1));
     d_psmice.alloc(size_t(2 * n) * L);
     d_pmaxerr.alloc(size_t(2 * n) * L);
     d_pcand.alloc(size_t(2 * n));
@@ -620,7 +833,7 @@ struct Engine::Impl {
     }
     const int tot = std::max(nphi * L, n * L * 3);
     prep_kernel<<<(tot + 255) / 256, 256, 0, stream>>>(n, L, nphi, d_prow_node.p, d_prow_phase.p, d_vhat.p, d_inj.p,
-                                                       d_vhatp.p, d_bv.p, d_iagg.p);
+                                                       d_vhatp.p, d_bv.p, d_iagg.p, d_iaggp.p);
     launched();
     CK(cudaGetLastError());
     build_z();
@@ -846,7 +1059,7 @@ struct Engine::Impl {
   void commit_device(int s, int r) {
     const unsigned ms = prob.mask[size_t(s)], mr = prob.mask[size_t(r)];
     commit_kernel<<<(L + 127) / 128, 128, 0, stream>>>(s, r, L, ms, mr, prow_off[size_t(s)], prow_off[size_t(r)],
-                                                       d_iagg.p, d_bv.p);
+                                                       d_iagg.p, d_bv.p, d_iaggp.p, nphi);
     launched();
     CK(cudaGetLastError());
     refresh_base();
@@ -892,6 +1105,23 @@ void Engine::solve(const double* inj, int nrhs, double* out) {
 }
 
 void Engine::loop_begin(const ReductionConfig& cfg) { impl_->begin(cfg); }
+
+void Engine::debug_base_refresh(int reps, double* ms, long long* clocks) {
+  Impl& I = *impl_;
+  DBuf<long long> dbg;
+  dbg.alloc(4);
+  CK(cudaMemset(dbg.p, 0, 4 * sizeof(long long)));
+  I.ensure_events();
+  I.refresh_base();
+  CK(cudaEventRecord(I.ev_a, I.stream));
+  for (int i = 0; i < reps; ++i) I.refresh_base();
+  *ms = I.event_ms() / reps;
+  I.dbg_clock = dbg.p;
+  I.refresh_base();
+  CK(cudaStreamSynchronize(I.stream));
+  I.dbg_clock = nullptr;
+  CK(cudaMemcpy(clocks, dbg.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost));
+}
 
 void Engine::set_scenarios(const std::vector<std::string>& ids, const std::vector<double>& inj,
                            const std::vector<double>& volt) {
@@ -1270,6 +1500,14 @@ extern "C" int krg_fp64_probe(int32_t device, double* gflops) {
     return status_from_current_exception();
   }
 }
+
+}  // namespace kronred::b200
+
+// debug/benchmark hook: time `reps` base refreshes (requires krg_loop_begin);
+// clocks[0..3] = block-0 warp-0 timestamps (start, forward, backward, output)
+extern "C" int krg_debug_base_refresh(krg_ctx* ctx, int32_t reps, double* ms, long long* clocks);
+
+namespace kronred::b200 {
 
 // self test: branch-free scorer sqrt vs __dsqrt_rn on n random inputs in [lo,hi)
 extern "C" int krg_selftest_sqrt(int64_t n, double lo, double hi, int64_t* mismatches) {

@@ -1,7 +1,12 @@
 // K1s (compact): anchored forward/backward sweeps on the present-phase
-// compacted factor, one right-hand side per CTA, the solution vector and —
-// when it fits — the whole factor and its level program staged in shared
-// memory, so a level costs shared-memory latency plus one __syncthreads.
+// compacted factor, one right-hand side per CTA. The right-hand side, the
+// solution, the factor and its level program all live in shared memory (when
+// they fit; the factor and program fall back to global/L1 otherwise), so a
+// level costs a few shared-memory round trips plus one __syncthreads.
+//
+// Level program: per step a packed record (solution offset, present-phase
+// count and mask, pinv offset, pull / coupling list) in level order, and per
+// pull or coupling a packed (offset, phase count, block offset) pair.
 //
 // Compaction is exact: a block's entries outside the present-phase rows/cols
 // are exact zeros, their products with finite operands are signed zeros, and
@@ -16,13 +21,9 @@ namespace {
 
 enum CMode { CM_FULL = 0, CM_BASE = 1, CM_ZCOL = 2 };
 
-// offsets into the packed int program
+// offsets (in ints) of the packed program sections
 struct CProg {
-  int st_x, st_m, st_mask, st_node, st_pinv;
-  int in_off, in_x, in_m, in_blk;
-  int cp_off, cp_x, cp_m, cp_blk;
-  int fw_off, fw, bw_off, bw;
-  int kept_x, kept_m, kept_i;
+  int frec, fent, brec, bent, fw_off, bw_off, kept;  // kept: (x | m << 24, kept index)
   int nsteps, nfw, nbw, nkept, nmeta, ncf, nphi;
 };
 
@@ -31,19 +32,21 @@ struct CSolveArgs {
   const int* meta_g;
   const double2* cfac_g;
   const double2* kept_val;  // [nkept][3] (present phases in order)
-  int smem_factor;          // stage cfac+meta in shared memory
-  // sources / sinks
-  int n;                    // nodes (MODE_FULL scatter)
+  int smem_factor;          // stage cfac + program in shared memory
+  int n;                    // nodes of this matrix
   const int* prow_off;      // [n+1]
   const std::uint8_t* mask; // [n]
-  const double2* rhs_full;  // [nrhs][3n] or null
-  double2* out_full;        // [nrhs][3n]
-  const double2* iagg;      // [n][L][3]
-  double2* base;            // bv: [nphi][L][2], base in slot 0
+  const int* prow_node;     // [nphi]
+  const std::uint8_t* prow_phase;
+  const double2* rhs_full;  // MODE_FULL: [nrhs][3n] or null
+  double2* out_full;        // MODE_FULL: [nrhs][3n]
+  const double2* iagg;      // MODE_BASE: [n][L][3]
+  double2* base;            // MODE_BASE: bv [nphi][L][2], base in slot 0
   int L;
-  int col0;
+  int col0;                 // MODE_ZCOL
   const double2* v0p;
   double2* zout;            // [ncol][nphi]
+  long long* dbg;           // optional phase timestamps (block 0, warp 0)
 };
 
 __device__ __forceinline__ int popc_below(unsigned m, int p) { return __popc(m & ((1u << p) - 1u)); }
@@ -52,7 +55,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) csolve_kernel(CSolveArgs a) {
   extern __shared__ double2 smem[];
   const CProg& P = a.P;
-  double2* x = smem;                                   // [nphi]
+  double2* x = smem;  // [nphi]: right-hand side, then t, then the solution
   const double2* cf = a.cfac_g;
   const int* M = a.meta_g;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -61,44 +64,49 @@ __global__ void __launch_bounds__(256) csolve_kernel(CSolveArgs a) {
     double2* scf = smem + P.nphi;
     int* smeta = reinterpret_cast<int*>(scf + P.ncf);
     for (int i = tid; i < P.ncf; i += nt) scf[i] = a.cfac_g[i];
-    for (int i = tid; i < P.nmeta; i += nt) smeta[i] = a.meta_g[i];
+    const int4* g4 = reinterpret_cast<const int4*>(a.meta_g);
+    int4* s4 = reinterpret_cast<int4*>(smeta);
+    for (int i = tid; i < (P.nmeta + 3) / 4; i += nt) s4[i] = g4[i];
     cf = scf;
     M = smeta;
-    __syncthreads();
   }
-  // boundary (kept) values
-  for (int k = tid; k < P.nkept; k += nt) {
-    const int x0 = M[P.kept_x + k], m = M[P.kept_m + k], ki = M[P.kept_i + k];
-    for (int i = 0; i < m; ++i) x[x0 + i] = a.kept_val[ki * 3 + i];
+  // right-hand side at present rows
+  for (int r = tid; r < P.nphi; r += nt) {
+    double2 b;
+    if (MODE == CM_BASE) {
+      b = a.iagg[(size_t(a.prow_node[r]) * a.L + rhs) * 3 + a.prow_phase[r]];
+    } else if (MODE == CM_ZCOL) {
+      b = (r == a.col0 + rhs) ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0);
+    } else {
+      b = a.rhs_full ? a.rhs_full[size_t(rhs) * 3 * a.n + size_t(a.prow_node[r]) * 3 + a.prow_phase[r]]
+                     : make_double2(0.0, 0.0);
+    }
+    x[r] = b;
   }
   __syncthreads();
+  // boundary (kept) values
+  for (int k = tid; k < P.nkept; k += nt) {
+    const int xe = M[P.kept + 2 * k], ki = M[P.kept + 2 * k + 1];
+    const int x0 = xe & 0xffffff, m = xe >> 24;
+    for (int i = 0; i < m; ++i) x[x0 + i] = a.kept_val[ki * 3 + i];
+  }
+  const int4* frec = reinterpret_cast<const int4*>(M + P.frec);
+  const int2* fent = reinterpret_cast<const int2*>(M + P.fent);
+  const int4* brec = reinterpret_cast<const int4*>(M + P.brec);
+  const int2* bent = reinterpret_cast<const int2*>(M + P.bent);
   // forward: rhs_k = b_k - sum_j A_kj t_j in elimination order; t_k = pinv_k rhs_k
   for (int lev = 0; lev < P.nfw; ++lev) {
     const int o0 = M[P.fw_off + lev], o1 = M[P.fw_off + lev + 1];
     for (int idx = o0 + tid; idx < o1; idx += nt) {
-      const int st = M[P.fw + idx];
-      const int xk = M[P.st_x + st], mk = M[P.st_m + st];
-      const unsigned msk = unsigned(M[P.st_mask + st]);
-      const int node = M[P.st_node + st];
-      C2 b[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const int4 rc = frec[idx];
+      const int xk = rc.x & 0xffffff, mk = (rc.x >> 24) & 3;
+      const int po = rc.z, e0 = rc.w & 0xffffff, ne = (rc.w >> 24) & 0xff;
+      C2 b[3];
 #pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        if (!((msk >> p) & 1u)) continue;
-        const int i = popc_below(msk, p);
-        C2 v;
-        if (MODE == CM_BASE) {
-          v = ld2(a.iagg + (size_t(node) * a.L + rhs) * 3 + p);
-        } else if (MODE == CM_ZCOL) {
-          v = (xk + i == a.col0 + rhs) ? C2{1.0, 0.0} : C2{0.0, 0.0};
-        } else {
-          v = a.rhs_full ? ld2(a.rhs_full + size_t(rhs) * 3 * a.n + size_t(node) * 3 + p) : C2{0.0, 0.0};
-        }
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (j == i) b[j] = v;
-      }
-      for (int e = M[P.in_off + st]; e < M[P.in_off + st + 1]; ++e) {
-        const int xj = M[P.in_x + e], mj = M[P.in_m + e], bo = M[P.in_blk + e];
+      for (int i = 0; i < 3; ++i) b[i] = i < mk ? ld2(x + xk + i) : C2{0.0, 0.0};
+      for (int e = e0; e < e0 + ne; ++e) {
+        const int2 en = fent[e];
+        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
         C2 tj[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) tj[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
@@ -112,7 +120,6 @@ __global__ void __launch_bounds__(256) csolve_kernel(CSolveArgs a) {
           b[r] = dev::csub(b[r], acc);
         }
       }
-      const int po = M[P.st_pinv + st];
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
         if (r >= mk) continue;
@@ -129,11 +136,13 @@ __global__ void __launch_bounds__(256) csolve_kernel(CSolveArgs a) {
   for (int lev = 0; lev < P.nbw; ++lev) {
     const int o0 = M[P.bw_off + lev], o1 = M[P.bw_off + lev + 1];
     for (int idx = o0 + tid; idx < o1; idx += nt) {
-      const int st = M[P.bw + idx];
-      const int xk = M[P.st_x + st], mk = M[P.st_m + st];
+      const int4 rc = brec[idx];
+      const int xk = rc.x & 0xffffff, mk = (rc.x >> 24) & 3;
+      const int po = rc.z, e0 = rc.w & 0xffffff, ne = (rc.w >> 24) & 0xff;
       C2 acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-      for (int e = M[P.cp_off + st]; e < M[P.cp_off + st + 1]; ++e) {
-        const int xj = M[P.cp_x + e], mj = M[P.cp_m + e], bo = M[P.cp_blk + e];
+      for (int e = e0; e < e0 + ne; ++e) {
+        const int2 en = bent[e];
+        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
         C2 xv[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) xv[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
@@ -147,7 +156,6 @@ __global__ void __launch_bounds__(256) csolve_kernel(CSolveArgs a) {
           acc[r] = dev::cadd(acc[r], u);
         }
       }
-      const int po = M[P.st_pinv + st];
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
         if (r >= mk) continue;
@@ -174,6 +182,373 @@ __global__ void __launch_bounds__(256) csolve_kernel(CSolveArgs a) {
       o[t] = ((m >> p) & 1u) ? x[a.prow_off[node] + popc_below(m, p)] : make_double2(0.0, 0.0);
     }
   }
+}
+
+// Warp-per-right-hand-side variant: the CTA stages the factor and program
+// into shared memory once; each warp then solves its own right-hand side with
+// __syncwarp between levels (no CTA barriers on the level-serial path).
+// W warps per CTA, solution vectors x[W][nphi] after the staged factor.
+template <int MODE, bool SMEMF>
+__global__ void __launch_bounds__(256) csolve_warp_kernel(CSolveArgs a, int nrhs) {
+  extern __shared__ double2 smem[];
+  const CProg& P = a.P;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int W = nt >> 5;
+  const int rhs = blockIdx.x * W + warp;
+  const double2* cf;
+  const int* M;
+  double2* xall;
+  if (SMEMF) {
+    double2* scf = smem;
+    int* smeta = reinterpret_cast<int*>(scf + P.ncf);
+    for (int i = tid; i < P.ncf; i += nt) scf[i] = a.cfac_g[i];
+    const int4* g4 = reinterpret_cast<const int4*>(a.meta_g);
+    int4* s4 = reinterpret_cast<int4*>(smeta);
+    for (int i = tid; i < (P.nmeta + 3) / 4; i += nt) s4[i] = g4[i];
+    cf = scf;
+    M = smeta;
+    xall = reinterpret_cast<double2*>(smeta + P.nmeta);
+    __syncthreads();
+  } else {
+    cf = a.cfac_g;
+    M = a.meta_g;
+    xall = smem;
+  }
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[0] = clock64();
+  if (rhs >= nrhs) return;
+  double2* x = xall + size_t(warp) * P.nphi;
+  for (int r = lane; r < P.nphi; r += 32) {
+    double2 b;
+    if (MODE == CM_BASE) {
+      b = a.iagg[(size_t(a.prow_node[r]) * a.L + rhs) * 3 + a.prow_phase[r]];
+    } else if (MODE == CM_ZCOL) {
+      b = (r == a.col0 + rhs) ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0);
+    } else {
+      b = a.rhs_full ? a.rhs_full[size_t(rhs) * 3 * a.n + size_t(a.prow_node[r]) * 3 + a.prow_phase[r]]
+                     : make_double2(0.0, 0.0);
+    }
+    x[r] = b;
+  }
+  __syncwarp();
+  for (int k = lane; k < P.nkept; k += 32) {
+    const int xe = M[P.kept + 2 * k], ki = M[P.kept + 2 * k + 1];
+    const int x0 = xe & 0xffffff, m = xe >> 24;
+    for (int i = 0; i < m; ++i) x[x0 + i] = a.kept_val[ki * 3 + i];
+  }
+  __syncwarp();
+  const int4* frec = reinterpret_cast<const int4*>(M + P.frec);
+  const int2* fent = reinterpret_cast<const int2*>(M + P.fent);
+  const int4* brec = reinterpret_cast<const int4*>(M + P.brec);
+  const int2* bent = reinterpret_cast<const int2*>(M + P.bent);
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[1] = clock64();
+  for (int lev = 0; lev < P.nfw; ++lev) {
+    const int o0 = M[P.fw_off + lev], o1 = M[P.fw_off + lev + 1];
+    for (int idx = o0 + lane; idx < o1; idx += 32) {
+      const int4 rc = frec[idx];
+      const int xk = rc.x & 0xffffff, mk = (rc.x >> 24) & 3;
+      const int po = rc.z, e0 = rc.w & 0xffffff, ne = (rc.w >> 24) & 0xff;
+      if (rc.x & (1 << 29)) {
+        // single-phase step with single-phase pulls: 1x1 complex blocks
+        C2 b = ld2(x + xk);
+        for (int e = e0; e < e0 + ne; ++e) {
+          const int2 en = fent[e];
+          const C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cmul(ld2(cf + en.y), ld2(x + (en.x & 0xffffff))));
+          b = dev::csub(b, acc);
+        }
+        st2(x + xk, dev::cadd(C2{0.0, 0.0}, dev::cmul(ld2(cf + po), b)));
+        continue;
+      }
+      C2 b[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) b[i] = i < mk ? ld2(x + xk + i) : C2{0.0, 0.0};
+      for (int e = e0; e < e0 + ne; ++e) {
+        const int2 en = fent[e];
+        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+        C2 tj[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tj[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          if (r >= mk) continue;
+          C2 acc = {0.0, 0.0};
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (c < mj) acc = dev::cadd(acc, dev::cmul(ld2(cf + bo + r * mj + c), tj[c]));
+          b[r] = dev::csub(b[r], acc);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (r >= mk) continue;
+        C2 acc = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (c < mk) acc = dev::cadd(acc, dev::cmul(ld2(cf + po + r * mk + c), b[c]));
+        st2(x + xk + r, acc);
+      }
+    }
+    __syncwarp();
+  }
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
+  for (int lev = 0; lev < P.nbw; ++lev) {
+    const int o0 = M[P.bw_off + lev], o1 = M[P.bw_off + lev + 1];
+    for (int idx = o0 + lane; idx < o1; idx += 32) {
+      const int4 rc = brec[idx];
+      const int xk = rc.x & 0xffffff, mk = (rc.x >> 24) & 3;
+      const int po = rc.z, e0 = rc.w & 0xffffff, ne = (rc.w >> 24) & 0xff;
+      if (rc.x & (1 << 29)) {
+        C2 acc = {0.0, 0.0};
+        for (int e = e0; e < e0 + ne; ++e) {
+          const int2 en = bent[e];
+          acc = dev::cadd(acc, dev::cadd(C2{0.0, 0.0}, dev::cmul(ld2(cf + en.y), ld2(x + (en.x & 0xffffff)))));
+        }
+        const C2 corr = dev::cadd(C2{0.0, 0.0}, dev::cmul(ld2(cf + po), acc));
+        st2(x + xk, dev::csub(ld2(x + xk), corr));
+        continue;
+      }
+      C2 acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int e = e0; e < e0 + ne; ++e) {
+        const int2 en = bent[e];
+        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+        C2 xv[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xv[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          if (r >= mk) continue;
+          C2 u = {0.0, 0.0};
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (c < mj) u = dev::cadd(u, dev::cmul(ld2(cf + bo + r * mj + c), xv[c]));
+          acc[r] = dev::cadd(acc[r], u);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (r >= mk) continue;
+        C2 corr = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (c < mk) corr = dev::cadd(corr, dev::cmul(ld2(cf + po + r * mk + c), acc[c]));
+        st2(x + xk + r, dev::csub(ld2(x + xk + r), corr));
+      }
+    }
+    __syncwarp();
+  }
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
+  if (MODE == CM_BASE) {
+    for (int r = lane; r < P.nphi; r += 32) a.base[(size_t(r) * a.L + rhs) * 2] = x[r];
+  } else if (MODE == CM_ZCOL) {
+    double2* zc = a.zout + size_t(a.col0 + rhs) * P.nphi;
+    for (int r = lane; r < P.nphi; r += 32) st2(zc + r, dev::csub(ld2(x + r), ld2(a.v0p + r)));
+  } else {
+    double2* o = a.out_full + size_t(rhs) * 3 * a.n;
+    for (int t = lane; t < 3 * a.n; t += 32) {
+      const int node = t / 3, p = t % 3;
+      const unsigned m = a.mask[node];
+      o[t] = ((m >> p) & 1u) ? x[a.prow_off[node] + popc_below(m, p)] : make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Base refresh (reduce.cpp:265-268), one warp per scenario. The factor, the
+// level program and each warp's right-hand side arrive in shared memory by
+// TMA bulk copies (cp.async.bulk + mbarrier transaction count). The program
+// is laid out in "lane slots": for every level round a record per lane, so a
+// round needs no level bounds and the next round's record is loaded while the
+// current one computes; single-phase steps with one pull/coupling carry it
+// inline. Per round the critical path is: x load -> complex chain -> store.
+//
+// record int4: x = x_k | m_k<<24 | SCALAR<<29 | INLINE<<30 | EMPTY<<31,
+//              y = pinv offset, z = inline ? x_j : first entry, w = inline ? block : count
+struct BaseArgs {
+  int nphi, ncf, nmeta, L, W;
+  int fslot, fext, nfr, bslot, bext, nbr, fent, bent, kept, nkept;  // program offsets (ints)
+  const double2* cfac;
+  const int* meta;
+  const double2* iaggp;   // [L][nphi]
+  const double2* kept_val;
+  double2* bv;            // [nphi][L][2], base in slot 0
+  long long* dbg;
+};
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(unsigned(__cvta_generic_to_shared(bar))), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(unsigned(__cvta_generic_to_shared(bar))),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(unsigned(__cvta_generic_to_shared(bar))),
+      "r"(parity));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   unsigned(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(bytes), "r"(unsigned(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+
+__device__ __forceinline__ C2 lds2(unsigned addr) {
+  double x, y;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
+  return {x, y};
+}
+__device__ __forceinline__ void sts2(unsigned addr, C2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+
+__global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ unsigned long long bar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rhs = blockIdx.x * a.W + warp;
+  const int nw = min(a.W, a.L - blockIdx.x * a.W);
+  double2* cf = smem;
+  int* M = reinterpret_cast<int*>(cf + a.ncf);
+  double2* xall = reinterpret_cast<double2*>(M + a.nmeta);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const unsigned bytes = unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u + unsigned(nw) * unsigned(a.nphi) * 16u;
+    mbar_expect_tx(&bar, bytes);
+    if (a.ncf) bulk_g2s(cf, a.cfac, unsigned(a.ncf) * 16u, &bar);
+    bulk_g2s(M, a.meta, unsigned(a.nmeta) * 4u, &bar);
+    for (int w = 0; w < nw; ++w)
+      bulk_g2s(xall + size_t(w) * a.nphi, a.iaggp + size_t(blockIdx.x * a.W + w) * a.nphi, unsigned(a.nphi) * 16u, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[0] = clock64();
+  if (warp >= nw) return;
+  double2* x = xall + size_t(warp) * a.nphi;
+  for (int k = lane; k < a.nkept; k += 32) {
+    const int xe = M[a.kept + 2 * k], ki = M[a.kept + 2 * k + 1];
+    const int x0 = xe & 0xffffff, m = xe >> 24;
+    for (int i = 0; i < m; ++i) x[x0 + i] = a.kept_val[ki * 3 + i];
+  }
+  __syncwarp();
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[1] = clock64();
+  // records: int4 {x_k*16 (<0: empty), pinv*16, x_j0*16, block0*16} (byte
+  // offsets into x / cf) + int4 {general?, m_k, first extra entry, extra count}.
+  // Scalar steps (one present phase, single-phase pulls) run one straight-line
+  // sequence on 32-bit shared addresses; the record arrays carry one padding
+  // round so the prefetch of round i+1 is unconditional.
+  const unsigned xs = unsigned(__cvta_generic_to_shared(x)), cs = unsigned(__cvta_generic_to_shared(cf));
+  const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
+  const int4* fx = reinterpret_cast<const int4*>(M + a.fext);
+  const int2* fe = reinterpret_cast<const int2*>(M + a.fent);
+  int4 rc = fs[lane];
+  int4 rx = fx[lane];
+  for (int fr = 0; fr < a.nfr; ++fr) {
+    const int4 nx = fs[(fr + 1) * 32 + lane];
+    const int4 nxx = fx[(fr + 1) * 32 + lane];
+    if (rc.x >= 0 && rx.x == 0) {
+      const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y);
+      C2 b = dev::csub(b0, dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj)));
+#pragma unroll 1
+      for (int e = rx.z; e < rx.z + rx.w; ++e) {
+        const int2 en = fe[e];
+        b = dev::csub(b, dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16))));
+      }
+      sts2(xs + rc.x, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, b)));
+    } else if (rc.x >= 0) {
+      const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
+      C2 b[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) b[i] = i < mk ? ld2(x + xk + i) : C2{0.0, 0.0};
+      for (int e = rx.z; e < rx.z + rx.w; ++e) {
+        const int2 en = fe[e];
+        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+        C2 tj[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) tj[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          if (r >= mk) continue;
+          C2 acc = {0.0, 0.0};
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (c < mj) acc = dev::cadd(acc, dev::cmul(ld2(cf + bo + r * mj + c), tj[c]));
+          b[r] = dev::csub(b[r], acc);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (r >= mk) continue;
+        C2 acc = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (c < mk) acc = dev::cadd(acc, dev::cmul(ld2(cf + po + r * mk + c), b[c]));
+        st2(x + xk + r, acc);
+      }
+    }
+    rc = nx;
+    rx = nxx;
+    __syncwarp();
+  }
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
+  const int4* bs = reinterpret_cast<const int4*>(M + a.bslot);
+  const int4* bx = reinterpret_cast<const int4*>(M + a.bext);
+  const int2* be = reinterpret_cast<const int2*>(M + a.bent);
+  rc = bs[lane];
+  rx = bx[lane];
+  for (int br = 0; br < a.nbr; ++br) {
+    const int4 nx = bs[(br + 1) * 32 + lane];
+    const int4 nxx = bx[(br + 1) * 32 + lane];
+    if (rc.x >= 0 && rx.x == 0) {
+      const C2 xj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y), t = lds2(xs + rc.x);
+      C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj)));
+#pragma unroll 1
+      for (int e = rx.z; e < rx.z + rx.w; ++e) {
+        const int2 en = be[e];
+        acc = dev::cadd(acc, dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16))));
+      }
+      sts2(xs + rc.x, dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc))));
+    } else if (rc.x >= 0) {
+      const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
+      C2 acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      for (int e = rx.z; e < rx.z + rx.w; ++e) {
+        const int2 en = be[e];
+        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+        C2 xv[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xv[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          if (r >= mk) continue;
+          C2 u = {0.0, 0.0};
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (c < mj) u = dev::cadd(u, dev::cmul(ld2(cf + bo + r * mj + c), xv[c]));
+          acc[r] = dev::cadd(acc[r], u);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (r >= mk) continue;
+        C2 corr = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (c < mk) corr = dev::cadd(corr, dev::cmul(ld2(cf + po + r * mk + c), acc[c]));
+        st2(x + xk + r, dev::csub(ld2(x + xk + r), corr));
+      }
+    }
+    rc = nx;
+    rx = nxx;
+    __syncwarp();
+  }
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
+  for (int r = lane; r < a.nphi; r += 32) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
 }
 
 // cfac[i] = (src >= 0 ? (src & 1 ? pinv : blocks)[src >> 1] : 0)

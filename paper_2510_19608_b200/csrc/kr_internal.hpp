@@ -156,6 +156,7 @@ class Engine {
 
   // loop parity hooks
   void loop_begin(const ReductionConfig& cfg);
+  void debug_base_refresh(int reps, double* ms, long long* clocks);
   std::int64_t loop_candidates(std::vector<int>& cs, std::vector<int>& cr);
   void loop_score_all(double* smice, std::uint8_t* feasible, double* max_err);
   void loop_best(krg_best* out, double* max_err);
