@@ -138,7 +138,7 @@ enum IntArr {
   A_APPLY_SLOTS, A_COUNT
 };
 
-constexpr int kTabPad = 64;  // row-table padding >= largest score_rows tile (S*T)
+constexpr int kTabPad = 64;  // row-table padding >= largest scorer tile (S*4 rows)
 
 struct Engine::Impl {
   Problem prob;
@@ -173,6 +173,7 @@ struct Engine::Impl {
   std::vector<int> sn_pos;     // compact index of each active super-node
   DBuf<double> d_psmice, d_pmaxerr, d_pcand, d_best;
   bool use_tiles = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) != "rows";
+  bool use_seg = std::getenv("KRONRED_SCORER") != nullptr && std::string(std::getenv("KRONRED_SCORER")) == "seg";
 
   // threads per scorer CTA: a multiple of L (whole candidates) and of 32
   int score_cta_threads() const {
@@ -702,6 +703,7 @@ struct Engine::Impl {
     for (auto fn : {score_kernel<false>, score_kernel<true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    CK(cudaFuncSetAttribute(score_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(base_refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     n = prob.y.n;
@@ -753,9 +755,9 @@ struct Engine::Impl {
     d_memlist.alloc(size_t(n));
     CK(cudaMallocHost(&h_cand, sizeof(int4) * size_t(2 * n)));
     CK(cudaMallocHost(&h_snt, sizeof(unsigned) * size_t(n)));
-    d_tab.alloc(size_t(nphi) + kTabPad);
+    d_tab.alloc(size_t(4) * n + size_t(nphi) + kTabPad);
     d_cidx.alloc(size_t(2 * n));
-    CK(cudaMallocHost(&h_tab, sizeof(unsigned) * (size_t(nphi) + kTabPad)));
+    CK(cudaMallocHost(&h_tab, sizeof(unsigned) * (size_t(4) * n + size_t(nphi) + kTabPad)));
     CK(cudaMallocHost(&h_cidx, sizeof(int) * size_t(2 * n)));
     tab_of_node.assign(size_t(n), -1);
     sn_pos.assign(size_t(n), -1);
@@ -848,10 +850,16 @@ struct Engine::Impl {
   void upload_iteration(long long c0, long long c1) {
     const long long C = c1 - c0;
     if (cfg.objective == Objective::magnitude) {
+      // 4-row blocks that never split a super-node; inert padding rows
+      // (phase field 3) fill each block
+      constexpr unsigned kPad = 7u;  // rho 0, first, phase 3
       int t = 0;
       for (int i : hs.supernodes) {
-        tab_of_node[size_t(i)] = t;
         const unsigned m = prob.mask[size_t(i)];
+        const int rows = __builtin_popcount(m);
+        if ((t & 3) + rows > 4)
+          while (t & 3) h_tab[t++] = kPad;
+        tab_of_node[size_t(i)] = t;
         unsigned first = 4u;
         for (int p = 0; p < 3; ++p)
           if ((m >> p) & 1u) {
@@ -860,8 +868,9 @@ struct Engine::Impl {
             first = 0u;
           }
       }
+      while (t & 3) h_tab[t++] = kPad;
       R = t;
-      for (int u = 0; u < kTabPad; ++u) h_tab[R + u] = R > 0 ? (h_tab[R - 1] & ~4u) : 0u;
+      for (int u = 0; u < kTabPad; ++u) h_tab[R + u] = kPad;
       int cnt[4] = {0, 0, 0, 0};
       for (long long c = c0; c < c1; ++c) ++cnt[__builtin_popcount(prob.mask[size_t(cr[size_t(c)])])];
       grp_off[0] = 0;
@@ -944,7 +953,41 @@ struct Engine::Impl {
       g.grp_cta[1] = (grp_off[1] - grp_off[0] + G - 1) / G;
       g.grp_cta[2] = g.grp_cta[1] + (grp_off[2] - grp_off[1] + G - 1) / G;
       g.grp_cta[3] = ctas;
-      if (ctas > 0 && use_tiles) {
+      if (ctas > 0 && use_seg) {
+        SegArgs q{};
+        q.C = int(C);
+        q.L = L;
+        q.nphi = nphi;
+        q.nblk = R / 4;
+        q.G = G;
+        // segments: enough warps to cover the device, P*S <= 512 threads
+        const long long pair_warps = (ctas * P + 31) / 32;
+        const long long want = (148LL * 24 + pair_warps - 1) / std::max(1LL, pair_warps);
+        int S2 = 1;
+        while (S2 * 2 <= want && P * S2 * 2 <= 512 && S2 < 16) S2 *= 2;
+        S2 = std::min(S2, std::max(1, (q.nblk + 1) / 2));
+        q.S = S2;
+        q.cand = d_cand.p;
+        q.cand_idx = d_cidx.p;
+        q.tab = d_tab.p;
+        q.mask = d_mask.p;
+        q.prow_off = d_prow_off.p;
+        q.Z = d_Z.p;
+        q.bv = d_bv.p;
+        q.iagg = d_iagg.p;
+        q.out_maxerr = d_pmaxerr.p;
+        q.out_cand = d_pcand.p;
+        q.e_bar = cfg.e_bar;
+        for (int k = 0; k < 4; ++k) {
+          q.grp_start[k] = g.grp_start[k];
+          q.grp_cta[k] = g.grp_cta[k];
+        }
+        const int Kr = 4 * S2;
+        const size_t buf_e = (size_t(Kr) * 4 + 15) / 16 + size_t(Kr) * L * 2 + size_t(G) * 3 * 2 * Kr;
+        const size_t smem = 2 * buf_e * 16 + 2 * size_t(Kr) * P * 8 + ((size_t(G) * 3 * 2 + 3) & ~size_t(3)) * 4 +
+                            size_t(std::max(S2, 2)) * P * 8 + 64;
+        score_seg_kernel<<<ctas, P * S2, smem, stream>>>(q);
+      } else if (ctas > 0 && use_tiles) {
         constexpr int K = 32;
         const size_t per_buf = (K * 4 + 15) / 16 + size_t(K) * L * 2 + size_t(G) * 3 * 2 * K;  // double2 units
         const size_t smem = std::max(2 * per_buf * sizeof(double2) + size_t(G) * 3 * 2 * sizeof(int) + 64,
