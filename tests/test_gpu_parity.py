@@ -183,3 +183,22 @@ def test_c2_benchmark_feeder_bitwise(tag, tmp_path):
     out = tmp_path / "r.json"
     res.write_reduced_json(str(out))
     assert out.read_text() == path("c2", f"reduced_{tag}.json").read_text()
+
+
+@pytest.mark.parametrize("tag,args", [("mag_1e-3", ["1e-3", "mag"]), ("complex_1e-3", ["1e-3", "complex"]),
+                                      ("rad_1e-2_t06", ["1e-2", "mag", "0.6", "--radialize"])])
+def test_cpp_dropin_cli_matches_reference_output(tag, args, tmp_path):
+    """The reference CLI's reduce command, relinked against this library,
+    writes the reference's reduced model byte for byte."""
+    import subprocess
+    from test_host import _build_dropin
+    exe = _build_dropin(tmp_path)
+    out = tmp_path / "reduced.json"
+    argv = [str(exe), str(path("c1", "net.json")), str(path("c1", "scen.csv"))] + args
+    while len(argv) < 7:
+        argv.append("-")
+    argv += [str(out), str(tmp_path / "trace.csv")]
+    if "--radialize" not in args:
+        argv[6] = "-"
+    subprocess.run(argv, check=True, capture_output=True)
+    assert out.read_text() == path("c1", f"reduced_{tag}.json").read_text()

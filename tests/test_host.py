@@ -134,3 +134,20 @@ def test_golden_runs_are_consistent():
             n = kr.HostProblem(str(path(case, "net.json"))).network.size
             for i, row in enumerate(rows):
                 assert row[4] == n - 1 - i
+
+
+def _build_dropin(tmp_path):
+    import subprocess
+    exe = tmp_path / "dropin_reduce"
+    lib = ROOT / "paper_2510_19608_b200" / "_lib"
+    kr.lib()  # builds the library if needed
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(ROOT / "tools" / "dropin_reduce.cpp"),
+                    f"-L{lib}", "-lkronred_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_dropin_compiles_against_header(tmp_path):
+    """tools/dropin_reduce.cpp is the reference CLI's cmd_reduce (main.cpp:52-120)
+    with only the include swapped; it must compile and link against the .so."""
+    exe = _build_dropin(tmp_path)
+    assert exe.exists()
