@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -73,6 +74,7 @@ struct DBuf {
 #include "kernels_elim.cuh"
 #include "kernels_csolve.cuh"
 #include "kernels_score.cuh"
+#include "kernels_loop.cuh"
 
 namespace kronred::b200 {
 namespace {
@@ -138,7 +140,7 @@ enum IntArr {
   A_APPLY_SLOTS, A_COUNT
 };
 
-constexpr int kTabPad = 64;  // row-table padding >= largest scorer tile (S*4 rows)
+constexpr int kTabPad = kTabPadRows;  // row-table padding >= largest scorer tile (S*4 rows)
 
 struct Engine::Impl {
   Problem prob;
@@ -197,6 +199,16 @@ struct Engine::Impl {
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_run0 = nullptr, ev_run1 = nullptr;
   KernelStats score_stats{}, solve_stats{};
   long long score_c0 = 0;
+  // device-resident loop (kernels_loop.cuh)
+  DBuf<LoopState> d_loopst;
+  DBuf<int> d_sup, d_sn, d_tabnode, d_cs, d_cr, d_brf, d_brt, d_trsr, d_trc;
+  DBuf<double> d_trsmice, d_trme;
+  DBuf<unsigned long long> d_trt;
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  DBuf<unsigned long long> d_tdbg;
+  bool loop_trace = std::getenv("KRONRED_LOOP_TRACE") != nullptr;
+  bool force_host_loop = std::getenv("KRONRED_LOOP") != nullptr && std::string(std::getenv("KRONRED_LOOP")) == "host";
 
   void launched() { ++launches; }
 
@@ -811,6 +823,9 @@ struct Engine::Impl {
     if (h_snt) cudaFreeHost(h_snt);
     if (h_tab) cudaFreeHost(h_tab);
     if (h_cidx) cudaFreeHost(h_cidx);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1099,6 +1114,238 @@ struct Engine::Impl {
     }
   }
 
+  // ---- device-resident loop ------------------------------------------------
+  static size_t pow2_at_least(size_t x) {
+    size_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+  }
+  size_t enum_smem() const { return pow2_at_least(std::max<size_t>(2 * prob.net.branches.size(), 1)) * sizeof(unsigned); }
+
+  bool device_loop_ok(const ReductionConfig& c) const {
+    return !force_host_loop && c.objective == Objective::magnitude && world == 1 && !profile && use_tiles &&
+           !use_seg && full.bW > 0 && n <= 65535 && enum_smem() + 24 * 1024 <= size_t(optin_smem);
+  }
+
+  LoopArgs loop_args() {
+    LoopArgs a{};
+    a.st = d_loopst.p;
+    a.n = n;
+    a.nb = int(prob.net.branches.size());
+    a.slack = prob.slack;
+    a.L = L;
+    a.nphi = nphi;
+    const int P = score_cta_threads();
+    a.G = (P % L == 0) ? P / L : 1;
+    a.cap = n;
+    a.has_target = cfg.target_reduction ? 1 : 0;
+    a.target = cfg.target_reduction ? *cfg.target_reduction : 0.0;
+    a.br_from = d_brf.p;
+    a.br_to = d_brt.p;
+    a.mask = d_mask.p;
+    a.prow_off = d_prow_off.p;
+    a.sup = d_sup.p;
+    a.sn = d_sn.p;
+    a.tab_of_node = d_tabnode.p;
+    a.tab = d_tab.p;
+    a.cs = d_cs.p;
+    a.cr = d_cr.p;
+    a.cand = d_cand.p;
+    a.cidx = d_cidx.p;
+    a.pcand = d_pcand.p;
+    a.pmaxerr = d_pmaxerr.p;
+    a.iagg = d_iagg.p;
+    a.bv = d_bv.p;
+    a.iaggp = d_iaggp.p;
+    a.tr_sr = d_trsr.p;
+    a.tr_c = d_trc.p;
+    a.tr_smice = d_trsmice.p;
+    a.tr_me = d_trme.p;
+    a.tr_t = d_trt.p;
+    return a;
+  }
+
+  // After begin(): runs every iteration on the device (one graph launch with
+  // a conditional WHILE node) and returns the committed trace.
+  void run_device_loop(std::vector<int>& tr_s, std::vector<int>& tr_r, std::vector<int>& tr_c,
+                       std::vector<double>& tr_smice, std::vector<double>& tr_me, std::vector<double>& tr_ms) {
+    const int nb = int(prob.net.branches.size());
+    if (!stream2) {
+      CK(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      CK(cudaFuncSetAttribute(enum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(enum_smem())));
+    }
+    d_loopst.alloc(1);
+    d_sup.alloc(size_t(n));
+    d_sn.alloc(size_t(n));
+    d_tabnode.alloc(size_t(n));
+    d_cs.alloc(size_t(2 * nb) + 1);
+    d_cr.alloc(size_t(2 * nb) + 1);
+    d_brf.alloc(size_t(nb) + 1);
+    d_brt.alloc(size_t(nb) + 1);
+    d_trsr.alloc(size_t(2 * n));
+    d_trc.alloc(size_t(n));
+    d_trsmice.alloc(size_t(n));
+    d_trme.alloc(size_t(n) * L);
+    d_trt.alloc(size_t(n) + 1);
+    d_cand.alloc(size_t(2 * nb) + 1);
+    d_cidx.alloc(size_t(2 * nb) + 1);
+    d_pcand.alloc(size_t(2 * nb) + 1);
+    d_pmaxerr.alloc((size_t(2 * nb) + 1) * L);
+    {
+      std::vector<int> ident(static_cast<size_t>(n)), bf(static_cast<size_t>(nb)), bt(static_cast<size_t>(nb));
+      std::iota(ident.begin(), ident.end(), 0);
+      for (int b = 0; b < nb; ++b) {
+        bf[size_t(b)] = prob.net.branches[size_t(b)].from;
+        bt[size_t(b)] = prob.net.branches[size_t(b)].to;
+      }
+      CK(cudaMemcpyAsync(d_sup.p, ident.data(), sizeof(int) * size_t(n), cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(d_sn.p, ident.data(), sizeof(int) * size_t(n), cudaMemcpyHostToDevice, stream));
+      if (nb) {
+        CK(cudaMemcpyAsync(d_brf.p, bf.data(), sizeof(int) * size_t(nb), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_brt.p, bt.data(), sizeof(int) * size_t(nb), cudaMemcpyHostToDevice, stream));
+      }
+      LoopState st0{};
+      st0.done = target_reached() ? 1 : 0;
+      st0.ns = n;
+      CK(cudaMemcpyAsync(d_loopst.p, &st0, sizeof st0, cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));  // host vectors go out of scope
+    }
+    LoopArgs la = loop_args();
+    if (loop_trace) {
+      d_tdbg.alloc(size_t(n + 1) * 8);
+      CK(cudaMemsetAsync(d_tdbg.p, 0, sizeof(unsigned long long) * size_t(n + 1) * 8, stream));
+      la.tdbg = d_tdbg.p;
+    }
+    // scorer launch (grid sized for the largest candidate set)
+    RowArgs g{};
+    g.L = L;
+    g.nphi = nphi;
+    g.tab = d_tab.p;
+    g.mask = d_mask.p;
+    g.prow_off = d_prow_off.p;
+    g.Z = d_Z.p;
+    g.bv = d_bv.p;
+    g.iagg = d_iagg.p;
+    g.out_smice = d_psmice.p;
+    g.out_maxerr = d_pmaxerr.p;
+    g.G = la.G;
+    g.S = 1;
+    g.cand = d_cand.p;
+    g.cand_idx = d_cidx.p;
+    g.out_cand = d_pcand.p;
+    g.e_bar = cfg.e_bar;
+    g.st = d_loopst.p;
+    g.tdbg = la.tdbg;
+    const int P = score_cta_threads();
+    constexpr int K = 32;
+    const size_t per_buf = (K * 4 + 15) / 16 + size_t(K) * L * 2 + size_t(la.G) * 3 * 2 * K;
+    const size_t score_smem = std::max(2 * per_buf * sizeof(double2) + size_t(la.G) * 3 * 2 * sizeof(int) + 64,
+                                       2 * size_t(P) * sizeof(double));
+    const int score_grid = (2 * nb + la.G - 1) / la.G + 3;
+    BaseArgs bb = full.bprog;
+    bb.L = L;
+    bb.W = full.bW;
+    bb.cfac = full.cfac.p;
+    bb.meta = full.bmeta.p;
+    bb.iaggp = d_iaggp.p;
+    bb.kept_val = d_slackv.p;
+    bb.bv = d_bv.p;
+    bb.dbg = nullptr;
+    bb.st = d_loopst.p;
+    bb.tdbg = la.tdbg;
+    // first enumeration (also stamps the loop start)
+    enum_kernel<<<1, kLoopThreads, enum_smem(), stream>>>(la);
+    launched();
+    CK(cudaGetLastError());
+    LoopState st{};
+    CK(cudaMemcpyAsync(&st, d_loopst.p, sizeof st, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (!st.done) {
+      cudaGraph_t graph;
+      CK(cudaGraphCreate(&graph, 0));
+      cudaGraphConditionalHandle h;
+      CK(cudaGraphConditionalHandleCreate(&h, graph, 1u, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp{};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cnode;
+      CK(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      LoopArgs lb = la;
+      lb.use_cond = 1;
+      lb.cond = h;
+      CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      score_tiles_kernel<<<score_grid, P, score_smem, stream>>>(g);
+      pick_commit_kernel<<<1, kLoopThreads, 0, stream>>>(lb);
+      CK(cudaEventRecord(ev_fork, stream));
+      CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
+      enum_kernel<<<1, kLoopThreads, enum_smem(), stream2>>>(lb);
+      base_refresh_kernel<<<(L + bb.W - 1) / bb.W, 32 * bb.W, full.bsmem, stream>>>(bb);
+      CK(cudaEventRecord(ev_join, stream2));
+      CK(cudaStreamWaitEvent(stream, ev_join, 0));
+      CK(cudaStreamEndCapture(stream, &body));
+      cudaGraphExec_t exec;
+      CK(cudaGraphInstantiate(&exec, graph, 0));
+      CK(cudaGraphLaunch(exec, stream));
+      CK(cudaStreamSynchronize(stream));
+      CK(cudaGraphExecDestroy(exec));
+      CK(cudaGraphDestroy(graph));
+      CK(cudaMemcpyAsync(&st, d_loopst.p, sizeof st, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      launches += 4LL * (st.iter + 1);
+    }
+    const int it = st.iter;
+    if (loop_trace && it > 2) {
+      std::vector<unsigned long long> T(size_t(n + 1) * 8);
+      CK(cudaMemcpy(T.data(), d_tdbg.p, sizeof(unsigned long long) * T.size(), cudaMemcpyDeviceToHost));
+      // per iteration i: score start [i][6], pick [i][0..1], enum for i+1 [i+1][2..3], refresh [i+1][4..5]
+      double a_sc = 0, a_pick = 0, a_p2e = 0, a_enum = 0, a_p2r = 0, a_r2s = 0, a_e2s = 0;
+      int cnt = 0;
+      for (int i = 1; i + 1 < it; ++i) {
+        const unsigned long long* c = &T[size_t(i) * 8];
+        const unsigned long long* nx = &T[size_t(i + 1) * 8];
+        a_sc += double(c[0] - c[6]);
+        a_pick += double(c[1] - c[0]);
+        a_p2e += double(nx[2] - c[1]);
+        a_enum += double(nx[3] - nx[2]);
+        a_p2r += double(nx[4] - c[1]);
+        a_r2s += double(nx[6] - nx[4]);
+        a_e2s += double(nx[6] - nx[3]);
+        ++cnt;
+      }
+      std::fprintf(stderr,
+                   "loop timeline (us/iter avg over %d): score+gap %.1f | pick %.1f | pick->enum %.1f enum %.1f | "
+                   "pick->refresh %.1f refresh-start->next score %.1f | enum-end->next score %.1f\n",
+                   cnt, a_sc / cnt / 1e3, a_pick / cnt / 1e3, a_p2e / cnt / 1e3, a_enum / cnt / 1e3, a_p2r / cnt / 1e3,
+                   a_r2s / cnt / 1e3, a_e2s / cnt / 1e3);
+    }
+    tr_s.resize(size_t(it));
+    tr_r.resize(size_t(it));
+    tr_c.resize(size_t(it));
+    tr_smice.resize(size_t(it));
+    tr_me.resize(size_t(it) * L);
+    tr_ms.assign(size_t(it), 0.0);
+    if (it > 0) {
+      std::vector<int> sr(static_cast<size_t>(2 * it));
+      std::vector<unsigned long long> tt(static_cast<size_t>(it));
+      CK(cudaMemcpyAsync(sr.data(), d_trsr.p, sizeof(int) * sr.size(), cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(tr_c.data(), d_trc.p, sizeof(int) * size_t(it), cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(tr_smice.data(), d_trsmice.p, sizeof(double) * size_t(it), cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(tr_me.data(), d_trme.p, sizeof(double) * tr_me.size(), cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(tt.data(), d_trt.p, sizeof(unsigned long long) * size_t(it), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      for (int i = 0; i < it; ++i) {
+        tr_s[size_t(i)] = sr[size_t(2 * i)];
+        tr_r[size_t(i)] = sr[size_t(2 * i + 1)];
+        if (i > 0) tr_ms[size_t(i)] = double(tt[size_t(i)] - tt[size_t(i - 1)]) * 1e-6;
+      }
+    }
+  }
+
   void commit_device(int s, int r) {
     const unsigned ms = prob.mask[size_t(s)], mr = prob.mask[size_t(r)];
     commit_kernel<<<(L + 127) / 128, 128, 0, stream>>>(s, r, L, ms, mr, prow_off[size_t(s)], prow_off[size_t(r)],
@@ -1336,7 +1583,29 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
   CK(cudaEventRecord(I.ev_run0, I.stream));
   I.begin(cfg);
   int iteration = 0;
-  while (!I.target_reached()) {
+  if (I.device_loop_ok(cfg)) {
+    // whole loop on the device; the host state machine replays the commits
+    // afterwards to rebuild clusters and call the observer in order
+    std::vector<int> ts, tr, tc;
+    std::vector<double> tsm, tme, tms;
+    I.run_device_loop(ts, tr, tc, tsm, tme, tms);
+    for (size_t i = 0; i < ts.size(); ++i) {
+      I.hs.commit(ts[i], tr[i]);
+      TraceRow row;
+      row.iteration = ++iteration;
+      row.s = ts[i];
+      row.r = tr[i];
+      row.smice = tsm[i];
+      row.max_err.assign(tme.begin() + long(i * size_t(I.L)), tme.begin() + long((i + 1) * size_t(I.L)));
+      row.supernode_count = int(I.hs.supernodes.size());
+      row.candidate_count = tc[i];
+      row.wall_ms = tms[i];
+      out.total_candidates += tc[i];
+      if (obs) obs(I.hs, row);
+      out.trace.push_back(std::move(row));
+    }
+  }
+  while (!I.device_loop_ok(cfg) && !I.target_reached()) {
     const auto t0 = std::chrono::steady_clock::now();
     I.hs.enumerate(I.cs, I.cr);
     const long long C = (long long)I.cs.size();

@@ -21,6 +21,15 @@ namespace {
 
 enum CMode { CM_FULL = 0, CM_BASE = 1, CM_ZCOL = 2 };
 
+// Device-resident loop state (kernels_loop.cuh): the iteration's sizes and
+// scorer grid layout, written by the enumeration kernel, read by the scorer,
+// the pick/commit kernel and the base refresh (which all exit when done).
+struct LoopState {
+  int done, iter, ns, C, R, err;
+  int grp_start[4];  // candidate offset of each |phi(r)| group (index 1..3)
+  int grp_cta[4];    // first CTA of each group; grp_cta[3] = CTAs in use
+};
+
 // offsets (in ints) of the packed program sections
 struct CProg {
   int frec, fent, brec, bent, fw_off, bw_off, kept;  // kept: (x | m << 24, kept index)
@@ -372,6 +381,8 @@ struct BaseArgs {
   const double2* kept_val;
   double2* bv;            // [nphi][L][2], base in slot 0
   long long* dbg;
+  const LoopState* st;    // device-resident loop: skip once the loop is done
+  unsigned long long* tdbg;  // optional loop timeline [iter][8] (slots 4, 5)
 };
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -410,6 +421,12 @@ __device__ __forceinline__ void sts2(unsigned addr, C2 v) {
 __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   __shared__ unsigned long long bar;
+  if (a.st && a.st->done) return;
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.tdbg[size_t(a.st->iter) * 8 + 4] = t;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rhs = blockIdx.x * a.W + warp;
   const int nw = min(a.W, a.L - blockIdx.x * a.W);

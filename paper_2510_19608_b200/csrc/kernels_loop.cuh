@@ -1,0 +1,379 @@
+// Device-resident iteration loop (magnitude objective, one GPU).
+//
+// The integer half of Algorithm 1 moves onto the device so that a whole
+// reduction runs as one CUDA graph with a conditional WHILE node and no host
+// round trip per iteration:
+//
+//   enum_kernel         enumerate_candidates (reduce.cpp:63-73) from the
+//                       super-node map: every branch (a,b) with sup[a] != sup[b]
+//                       is a super-node edge (a contracted tree has no parallel
+//                       edges); both directions are filtered (r != slack,
+//                       phi(r) subset of phi(s)) and sorted lexicographically
+//                       (bitonic sort of (s << 16 | r) keys in shared memory).
+//                       It also lays out the scorer's row table: active
+//                       super-nodes ascending, rows in 4-row blocks that never
+//                       split a super-node (a 4-state transducer, scanned over
+//                       the block), and groups the candidates by |phi(r)|.
+//   pick_commit_kernel  the argmin (reduce.cpp:397-404: first minimum SMICE among
+//                       feasible candidates), the trace row, and commit
+//                       (reduce.cpp:299-344): i_agg move, cluster bound merge,
+//                       super-node map relabel, removal of r from the active
+//                       list, target test (reduce.cpp:369-373).
+//
+// Every kernel of the loop body returns immediately once st->done is set;
+// enum_kernel sets the graph's loop condition.
+#pragma once
+
+namespace kronred::b200 {
+namespace {
+
+struct LoopArgs {
+  LoopState* st;
+  int n, nb, slack, L, nphi, G, cap;
+  int has_target;
+  double target;
+  const int* br_from;
+  const int* br_to;
+  const std::uint8_t* mask;
+  const int* prow_off;
+  int* sup;            // [n] super-node of every original node
+  int* sn;             // [n] active super-nodes, ascending (st->ns of them)
+  int* tab_of_node;    // [n] first table row of each active super-node
+  unsigned* tab;       // [4n + pad] row table
+  int* cs;             // [2n] candidates, lexicographic
+  int* cr;
+  int4* cand;          // [2n] grouped by |phi(r)|: (s, r, tab(s), tab(r))
+  int* cidx;           // [2n] lexicographic index of each grouped slot
+  const double* pcand; // [C] SMICE or -1 (infeasible), lexicographic index
+  const double* pmaxerr;
+  double2* iagg;       // [n][L][3]
+  double2* bv;         // [nphi][L][2]
+  double2* iaggp;      // [L][nphi]
+  int* tr_sr;          // [cap][2]
+  int* tr_c;           // [cap]
+  double* tr_smice;    // [cap]
+  double* tr_me;       // [cap][L]
+  unsigned long long* tr_t;  // [cap] globaltimer at commit
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+  unsigned long long* tdbg;  // optional timeline [iter][8]: pick start/end, enum start/end
+};
+
+constexpr unsigned kPadEntry = 7u;  // rho 0, first, phase 3 (inert row)
+constexpr int kTabPadRows = 64;    // row-table padding >= largest scorer tile
+constexpr int kLoopThreads = 1024;
+
+// 4-state transducer of the row-table layout: state q = rows mod 4 so far.
+// A super-node with k rows that does not fit the current block is pushed to
+// the next one (4 - q padding rows).
+__device__ __forceinline__ void tab_step(int k, int& q, int& adv) {
+  if (q + k > 4) {
+    adv += 4 - q + k;
+    q = k & 3;
+  } else {
+    adv += k;
+    q = (q + k) & 3;
+  }
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
+  extern __shared__ unsigned keys[];  // [pow2 >= 2n]
+  __shared__ int s_cnt;
+  __shared__ unsigned char mq[kLoopThreads][4];
+  __shared__ int ma[kLoopThreads][4];
+  __shared__ unsigned long long gscan[kLoopThreads / 32];
+  LoopState* st = a.st;
+  const int tid = threadIdx.x;
+  if (st->done) {
+    if (a.use_cond && tid == 0) cudaGraphSetConditional(a.cond, 0u);
+    return;
+  }
+  const int ns = st->ns;
+  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * 8 + 2] = globaltimer();
+
+  // ---- row table over the active super-nodes ------------------------------
+  const int ch = (ns + kLoopThreads - 1) / kLoopThreads;
+  const int b0 = min(ns, tid * ch), b1 = min(ns, b0 + ch);
+  for (int q0 = 0; q0 < 4; ++q0) {
+    int q = q0, adv = 0;
+    for (int k = b0; k < b1; ++k) tab_step(__popc(a.mask[a.sn[k]]), q, adv);
+    mq[tid][q0] = (unsigned char)q;
+    ma[tid][q0] = adv;
+  }
+  __syncthreads();
+  // inclusive Hillis-Steele scan of map composition (earlier map first)
+  for (int d = 1; d < kLoopThreads; d <<= 1) {
+    unsigned char nq[4];
+    int na[4];
+    const bool act = tid >= d;
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int q1 = mq[tid - d][q];
+        nq[q] = mq[tid][q1];
+        na[q] = ma[tid - d][q] + ma[tid][q1];
+      }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        mq[tid][q] = nq[q];
+        ma[tid][q] = na[q];
+      }
+    }
+    __syncthreads();
+  }
+  {
+    int q = tid == 0 ? 0 : mq[tid - 1][0];
+    int t = tid == 0 ? 0 : ma[tid - 1][0];
+    for (int k = b0; k < b1; ++k) {
+      const int i = a.sn[k];
+      const unsigned m = a.mask[i];
+      const int rows = __popc(m);
+      if (q + rows > 4) {
+        for (int u = q; u < 4; ++u) a.tab[t++] = kPadEntry;
+        q = 0;
+      }
+      a.tab_of_node[i] = t;
+      unsigned first = 4u;
+      int rho = a.prow_off[i];
+      for (int p = 0; p < 3; ++p)
+        if ((m >> p) & 1u) {
+          a.tab[t++] = (unsigned(rho++) << 3) | first | unsigned(p);
+          first = 0u;
+        }
+      q = (q + rows) & 3;
+    }
+    if (tid == kLoopThreads - 1) {
+      // tail: close the last block and add the scorer's tile padding
+      const int tend = ma[kLoopThreads - 1][0];
+      const int R = (tend + 3) & ~3;
+      for (int u = tend; u < R + kTabPadRows; ++u) a.tab[u] = kPadEntry;
+      st->R = R;
+    }
+  }
+
+  // ---- candidates: super-node edges, both directions, filtered ------------
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  for (int b = tid; b < a.nb; b += kLoopThreads) {
+    const int x = a.sup[a.br_from[b]], y = a.sup[a.br_to[b]];
+    if (x == y) continue;
+    const unsigned mx = a.mask[x], my = a.mask[y];
+    if (y != a.slack && (my & ~mx) == 0u) keys[atomicAdd(&s_cnt, 1)] = (unsigned(x) << 16) | unsigned(y);
+    if (x != a.slack && (mx & ~my) == 0u) keys[atomicAdd(&s_cnt, 1)] = (unsigned(y) << 16) | unsigned(x);
+  }
+  __syncthreads();
+  const int C = s_cnt;
+  if (C == 0) {
+    if (tid == 0) {
+      st->C = 0;
+      st->done = 1;
+      if (a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+    }
+    return;
+  }
+  int N = 1;
+  while (N < C) N <<= 1;
+  for (int i = C + tid; i < N; i += kLoopThreads) keys[i] = 0xffffffffu;
+  __syncthreads();
+  for (int k = 2; k <= N; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < N; i += kLoopThreads) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned ki = keys[i], kl = keys[l];
+          const bool up = (i & k) == 0;
+          if ((ki > kl) == up) {
+            keys[i] = kl;
+            keys[l] = ki;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = tid; i < C; i += kLoopThreads) {
+    a.cs[i] = int(keys[i] >> 16);
+    a.cr[i] = int(keys[i] & 0xffffu);
+  }
+
+  // ---- group by |phi(r)| (stable): packed 3 x 21-bit counters, block scan --
+  const int cch = (C + kLoopThreads - 1) / kLoopThreads;
+  const int c0 = min(C, tid * cch), c1 = min(C, c0 + cch);
+  unsigned long long mine = 0;
+  for (int i = c0; i < c1; ++i) mine += 1ull << (21 * (__popc(a.mask[keys[i] & 0xffffu]) - 1));
+  // exclusive block scan of `mine`
+  unsigned long long incl = mine;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) gscan[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = gscan[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += v;
+    }
+    gscan[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  const unsigned long long total = gscan[kLoopThreads / 32 - 1];
+  const unsigned long long excl = incl - mine + (warp > 0 ? gscan[warp - 1] : 0ull);
+  const int cnt1 = int(total & 0x1fffff), cnt2 = int((total >> 21) & 0x1fffff);
+  int pos[4] = {0, 0, cnt1, cnt1 + cnt2};
+  pos[1] += int(excl & 0x1fffff);
+  pos[2] += int((excl >> 21) & 0x1fffff);
+  pos[3] += int((excl >> 42) & 0x1fffff);
+  for (int i = c0; i < c1; ++i) {
+    const int s = int(keys[i] >> 16), r = int(keys[i] & 0xffffu);
+    const int g = __popc(a.mask[r]);
+    const int p = pos[g]++;
+    a.cand[p] = make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
+    a.cidx[p] = i;
+  }
+  if (tid == 0) {
+    const int cnt3 = C - cnt1 - cnt2;
+    st->C = C;
+    st->grp_start[0] = 0;
+    st->grp_start[1] = 0;
+    st->grp_start[2] = cnt1;
+    st->grp_start[3] = cnt1 + cnt2;
+    st->grp_cta[0] = 0;
+    st->grp_cta[1] = (cnt1 + a.G - 1) / a.G;
+    st->grp_cta[2] = st->grp_cta[1] + (cnt2 + a.G - 1) / a.G;
+    st->grp_cta[3] = st->grp_cta[2] + (cnt3 + a.G - 1) / a.G;
+    if (a.use_cond) cudaGraphSetConditional(a.cond, 1u);
+    if (a.tdbg) a.tdbg[size_t(st->iter) * 8 + 3] = globaltimer();
+  }
+}
+
+__device__ __forceinline__ bool loop_better(double s1, int i1, double s2, int i2) {
+  if (i1 < 0) return false;
+  if (i2 < 0) return true;
+  return s1 < s2 || (s1 == s2 && i1 < i2);
+}
+
+__global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
+  __shared__ double ss[32];
+  __shared__ int si[32];
+  __shared__ int s_pos;
+  LoopState* st = a.st;
+  if (st->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int C = st->C;
+  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * 8 + 0] = globaltimer();
+  double bs = __longlong_as_double(0x7ff0000000000000LL);
+  int bi = -1;
+  for (int c = tid; c < C; c += kLoopThreads) {
+    const double v = a.pcand[c];
+    if (!(v < 0.0) && loop_better(v, c, bs, bi)) {
+      bs = v;
+      bi = c;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double os = __shfl_down_sync(0xffffffffu, bs, o);
+    const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+    if (loop_better(os, oi, bs, bi)) {
+      bs = os;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    ss[warp] = bs;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    bs = ss[lane];
+    bi = si[lane];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double os = __shfl_down_sync(0xffffffffu, bs, o);
+      const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (loop_better(os, oi, bs, bi)) {
+        bs = os;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      ss[0] = bs;
+      si[0] = bi;
+    }
+  }
+  __syncthreads();
+  bi = si[0];
+  bs = ss[0];
+  if (bi < 0) {  // no feasible assignment left (reduce.cpp:404)
+    if (tid == 0) st->done = 1;
+    return;
+  }
+  const int it = st->iter;
+  const int s = a.cs[bi], r = a.cr[bi];
+  const int L = a.L;
+  if (it < a.cap) {
+    if (tid == 0) {
+      a.tr_sr[2 * it] = s;
+      a.tr_sr[2 * it + 1] = r;
+      a.tr_c[it] = C;
+      a.tr_smice[it] = bs;
+      a.tr_t[it] = globaltimer();
+    }
+    for (int l = tid; l < L; l += kLoopThreads) a.tr_me[size_t(it) * L + l] = a.pmaxerr[size_t(bi) * L + l];
+  }
+  // i_agg[s] += i_agg[r], i_agg[r] = 0 (reduce.cpp:336-343); bounds merge
+  const unsigned ms = a.mask[s], mr = a.mask[r];
+  const int rs0 = a.prow_off[s], rr0 = a.prow_off[r];
+  for (int l = tid; l < L; l += kLoopThreads) {
+    for (int p = 0; p < 3; ++p) {
+      double2* ps = a.iagg + (size_t(s) * L + l) * 3 + p;
+      double2* pr = a.iagg + (size_t(r) * L + l) * 3 + p;
+      const C2 sum = dev::cadd(ld2(ps), ld2(pr));
+      st2(ps, sum);
+      *pr = make_double2(0.0, 0.0);
+      if ((ms >> p) & 1u) st2(a.iaggp + size_t(l) * a.nphi + rs0 + popc_below(ms, p), sum);
+      if ((mr >> p) & 1u) {
+        a.iaggp[size_t(l) * a.nphi + rr0 + popc_below(mr, p)] = make_double2(0.0, 0.0);
+        double2* dst = a.bv + (size_t(rs0 + popc_below(ms, p)) * L + l) * 2 + 1;
+        const double2 bb = a.bv[(size_t(rr0 + popc_below(mr, p)) * L + l) * 2 + 1];
+        const double2 cur = *dst;
+        *dst = make_double2(dmin(cur.x, bb.x), dmax(cur.y, bb.y));
+      }
+    }
+  }
+  for (int j = tid; j < a.n; j += kLoopThreads)
+    if (a.sup[j] == r) a.sup[j] = s;
+  // remove r from the ascending active list
+  const int ns = st->ns;
+  for (int k = tid; k < ns; k += kLoopThreads)
+    if (a.sn[k] == r) s_pos = k;
+  __syncthreads();
+  // shift the tail left by one, a block-wide chunk at a time (each chunk is
+  // read completely before any of it is written)
+  for (int base = s_pos + 1; base < ns; base += kLoopThreads) {
+    const int k = base + tid;
+    const int v = k < ns ? a.sn[k] : 0;
+    __syncthreads();
+    if (k < ns) a.sn[k - 1] = v;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    st->ns = ns - 1;
+    st->iter = it + 1;
+    if (a.has_target && double(a.n - (ns - 1)) / double(a.n) >= a.target) st->done = 1;
+    if (it + 1 >= a.cap) st->done = 1;
+    if (a.tdbg) a.tdbg[size_t(it) * 8 + 1] = globaltimer();
+  }
+}
+
+}  // namespace
+}  // namespace kronred::b200
