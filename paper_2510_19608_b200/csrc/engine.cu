@@ -74,6 +74,7 @@ struct DBuf {
 #include "kernels_elim.cuh"
 #include "kernels_csolve.cuh"
 #include "kernels_score.cuh"
+#include "kernels_score2.cuh"
 #include "kernels_loop.cuh"
 
 namespace kronred::b200 {
@@ -175,6 +176,8 @@ struct Engine::Impl {
   std::vector<int> sn_pos;     // compact index of each active super-node
   DBuf<double> d_psmice, d_pmaxerr, d_pcand, d_best;
   bool use_tiles = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) != "rows";
+  // score2 (kernels_score2.cuh) is the default; KRONRED_SCORER=tiles|seg|rows select the older variants
+  bool use_score2 = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) == "score2";
   bool use_seg = std::getenv("KRONRED_SCORER") != nullptr && std::string(std::getenv("KRONRED_SCORER")) == "seg";
 
   // threads per scorer CTA: a multiple of L (whole candidates) and of 32
@@ -715,6 +718,7 @@ struct Engine::Impl {
     for (auto fn : {score_kernel<false>, score_kernel<true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    CK(cudaFuncSetAttribute(score2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(base_refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
@@ -1002,6 +1006,9 @@ struct Engine::Impl {
         const size_t smem = 2 * buf_e * 16 + 2 * size_t(Kr) * P * 8 + ((size_t(G) * 3 * 2 + 3) & ~size_t(3)) * 4 +
                             size_t(std::max(S2, 2)) * P * 8 + 64;
         score_seg_kernel<<<ctas, P * S2, smem, stream>>>(q);
+      } else if (ctas > 0 && use_score2) {
+        const size_t smem = Score2Layout{L, G, 3}.smem_bytes(P);
+        score2_kernel<<<ctas, P, smem, stream>>>(g);
       } else if (ctas > 0 && use_tiles) {
         constexpr int K = 32;
         const size_t per_buf = (K * 4 + 15) / 16 + size_t(K) * L * 2 + size_t(G) * 3 * 2 * K;  // double2 units
@@ -1279,7 +1286,10 @@ struct Engine::Impl {
       lb.use_cond = 1;
       lb.cond = h;
       CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-      score_tiles_kernel<<<score_grid, P, score_smem, stream>>>(g);
+      if (use_score2)
+        score2_kernel<<<score_grid, P, Score2Layout{L, la.G, 3}.smem_bytes(P), stream>>>(g);
+      else
+        score_tiles_kernel<<<score_grid, P, score_smem, stream>>>(g);
       pick_commit_kernel<<<1, kLoopThreads, 0, stream>>>(lb);
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
