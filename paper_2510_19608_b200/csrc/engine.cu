@@ -75,6 +75,7 @@ struct DBuf {
 #include "kernels_csolve.cuh"
 #include "kernels_score.cuh"
 #include "kernels_score2.cuh"
+#include "kernels_score3.cuh"
 #include "kernels_loop.cuh"
 
 namespace kronred::b200 {
@@ -175,9 +176,40 @@ struct Engine::Impl {
   int grp_off[4] = {0, 0, 0, 0};
   std::vector<int> sn_pos;     // compact index of each active super-node
   DBuf<double> d_psmice, d_pmaxerr, d_pcand, d_best;
+  DBuf<int> d_grpdone;  // score3 slice-completion counters
   bool use_tiles = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) != "rows";
   // score2 (kernels_score2.cuh) is the default; KRONRED_SCORER=tiles|seg|rows select the older variants
-  bool use_score2 = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) == "score2";
+  bool use_score3 = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) == "score3";
+  bool use_score2 = std::getenv("KRONRED_SCORER") != nullptr && std::string(std::getenv("KRONRED_SCORER")) == "score2";
+  // score3 geometry: 16 Z-column slots per CTA, scenario slices of up to 8
+  static constexpr int kS3Slots = 16;
+  int s3_ls() const { return std::min(L, 8); }
+  int s3_ldc() const { return std::max(2 * n, 2 * int(prob.net.branches.size()) + 1); }
+  int s3_nsl() const { return (L + s3_ls() - 1) / s3_ls(); }
+  int s3_threads() const { return (kS3Slots * s3_ls() + 31) / 32 * 32; }
+  S3Args s3_args() const {
+    S3Args q{};
+    q.L = L;
+    q.nphi = nphi;
+    q.G = kS3Slots;
+    q.Ls = s3_ls();
+    q.nsl = s3_nsl();
+    q.cand = d_cand.p;
+    q.cand_idx = d_cidx.p;
+    q.tab = d_tab.p;
+    q.mask = d_mask.p;
+    q.prow_off = d_prow_off.p;
+    q.Z = d_Z.p;
+    q.bv = d_bv.p;
+    q.iagg = d_iagg.p;
+    q.out_sm = d_psmice.p;
+    q.out_mx = d_pmaxerr.p;
+    q.ldc = s3_ldc();
+    q.e_bar = cfg.e_bar;
+    q.out_cand = d_pcand.p;
+    q.grp_done = d_grpdone.p;
+    return q;
+  }
   bool use_seg = std::getenv("KRONRED_SCORER") != nullptr && std::string(std::getenv("KRONRED_SCORER")) == "seg";
 
   // threads per scorer CTA: a multiple of L (whole candidates) and of 32
@@ -443,10 +475,23 @@ struct Engine::Impl {
               for (int e = 0; e < ne; ++e) scalar = scalar && (ex[size_t(first + e)] >> 24) == 1;
               if (size_t(d.xoff[size_t(nn)]) * 16 >= (1u << 31) || size_t(g.size()) * 16 >= (1u << 31))
                 throw Error("base program offsets overflow");
-              if (scalar) {
-                // first pull inline; a pull-free step gets an exact-zero pull
-                // (b - (0 + 0*x) == b bit for bit), so every scalar step runs
-                // the same instruction sequence
+              if (scalar && fwd) {
+                // forward: the first two pulls inline; missing pulls are exact
+                // zero pulls (b - (0 + 0*x) == b bit for bit), so every scalar
+                // step runs the same instruction sequence with both products
+                // in flight at once
+                const int xj = ne == 0 ? d.xoff[size_t(k)] : (ex[size_t(first)] & 0xffffff);
+                const int bo = ne == 0 ? zero_cf : eb[size_t(first)];
+                const int xj1 = ne < 2 ? d.xoff[size_t(k)] : (ex[size_t(first + 1)] & 0xffffff);
+                const int bo1 = ne < 2 ? zero_cf : eb[size_t(first + 1)];
+                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, xj * 16, bo * 16});
+                ext.insert(ext.end(), {xj1 * 16, bo1 * 16, int(ents.size() / 2), std::max(ne - 2, 0)});
+                for (int e = 2; e < ne; ++e) {
+                  ents.push_back(ex[size_t(first + e)]);
+                  ents.push_back(eb[size_t(first + e)]);
+                }
+              } else if (scalar) {
+                // backward: first coupling inline (an exact-zero one when none)
                 const int xj = ne == 0 ? d.xoff[size_t(k)] : (ex[size_t(first)] & 0xffffff);
                 const int bo = ne == 0 ? zero_cf : eb[size_t(first)];
                 recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, xj * 16, bo * 16});
@@ -456,7 +501,7 @@ struct Engine::Impl {
                   ents.push_back(eb[size_t(first + e)]);
                 }
               } else {
-                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, 0, 0});
+                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, fwd ? -1 : 0, 0});
                 ext.insert(ext.end(), {1, mk, int(ents.size() / 2), ne});
                 for (int e = 0; e < ne; ++e) {
                   ents.push_back(ex[size_t(first + e)]);
@@ -719,6 +764,7 @@ struct Engine::Impl {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
+    CK(cudaFuncSetAttribute(score3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 256));
     CK(cudaFuncSetAttribute(score_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(base_refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
@@ -807,8 +853,10 @@ struct Engine::Impl {
     d_bv.alloc(size_t(nphi) * L * 2);
     d_iagg.alloc(size_t(n) * L * 3);
     d_iaggp.alloc(size_t(L) * std::max(nphi, 1));
-    d_psmice.alloc(size_t(2 * n) * L);
-    d_pmaxerr.alloc(size_t(2 * n) * L);
+    d_psmice.alloc(size_t(s3_ldc()) * L);
+    d_pmaxerr.alloc(size_t(s3_ldc()) * L);
+    d_grpdone.alloc(size_t(s3_ldc()) / 4 + 8);
+    CK(cudaMemset(d_grpdone.p, 0, d_grpdone.n * sizeof(int)));
     d_pcand.alloc(size_t(2 * n));
     d_best.alloc(size_t(2 + L));
     if (h_best) cudaFreeHost(h_best);
@@ -1006,6 +1054,22 @@ struct Engine::Impl {
         const size_t smem = 2 * buf_e * 16 + 2 * size_t(Kr) * P * 8 + ((size_t(G) * 3 * 2 + 3) & ~size_t(3)) * 4 +
                             size_t(std::max(S2, 2)) * P * 8 + 64;
         score_seg_kernel<<<ctas, P * S2, smem, stream>>>(q);
+      } else if (ctas > 0 && use_score3) {
+        S3Args q = s3_args();
+        q.C = int(C);
+        q.R = R;
+        int c3 = 0;
+        for (int k = 1; k <= 3; ++k) {
+          q.grp_start[k] = grp_off[k - 1];
+          q.grp_cta[k - 1] = c3;
+          const int cpc = kS3Slots / k;
+          c3 += (grp_off[k] - grp_off[k - 1] + cpc - 1) / cpc * q.nsl;
+        }
+        q.grp_cta[1] = (grp_off[1] - grp_off[0] + kS3Slots - 1) / kS3Slots * q.nsl;
+        q.grp_cta[2] = q.grp_cta[1] + (grp_off[2] - grp_off[1] + kS3Slots / 2 - 1) / (kS3Slots / 2) * q.nsl;
+        q.grp_cta[3] = c3;
+        if (c3 > 0)
+          score3_kernel<<<c3, s3_threads(), S3Layout{s3_ls(), kS3Slots}.smem_bytes(), stream>>>(q);
       } else if (ctas > 0 && use_score2) {
         const size_t smem = Score2Layout{L, G, 3}.smem_bytes(P);
         score2_kernel<<<ctas, P, smem, stream>>>(g);
@@ -1078,7 +1142,7 @@ struct Engine::Impl {
     score_c0 = c0;
     upload_iteration(c0, c1);
     launch_score(C);
-    argmin_kernel<<<1, 1024, 0, stream>>>(int(std::max(C, 0LL)), L, cfg.e_bar, c0, d_psmice.p, d_pmaxerr.p,
+    argmin_kernel<<<1, 1024, 0, stream>>>(int(std::max(C, 0LL)), L, (cfg.objective == Objective::magnitude && use_score3) ? s3_ldc() : 0, cfg.e_bar, c0, d_psmice.p, d_pmaxerr.p,
                                           cfg.objective == Objective::magnitude ? d_pcand.p : nullptr,
                                           d_best.p);
     launched();
@@ -1145,6 +1209,14 @@ struct Engine::Impl {
     const int P = score_cta_threads();
     a.G = (P % L == 0) ? P / L : 1;
     a.cap = n;
+    a.e_bar = cfg.e_bar;
+    a.nsl = 1;
+    for (int k = 1; k <= 3; ++k) a.cpc[k] = a.G;
+    if (use_score3) {
+      a.nsl = s3_nsl();
+      for (int k = 1; k <= 3; ++k) a.cpc[k] = kS3Slots / k;
+      a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
+    }
     a.has_target = cfg.target_reduction ? 1 : 0;
     a.target = cfg.target_reduction ? *cfg.target_reduction : 0.0;
     a.br_from = d_brf.p;
@@ -1286,7 +1358,19 @@ struct Engine::Impl {
       lb.use_cond = 1;
       lb.cond = h;
       CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-      if (use_score2)
+      if (use_score3) {
+        S3Args q = s3_args();
+        q.st = d_loopst.p;
+        q.tdbg = la.tdbg;
+        int occ = 0;
+        const size_t sm3 = S3Layout{s3_ls(), kS3Slots}.smem_bytes();
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score3_kernel, s3_threads(), sm3));
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        const int items_max = ((2 * nb + 4) / 5 + 3) * s3_nsl();
+        const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
+        score3_kernel<<<grid3, s3_threads(), sm3, stream>>>(q);
+      } else if (use_score2)
         score2_kernel<<<score_grid, P, Score2Layout{L, la.G, 3}.smem_bytes(P), stream>>>(g);
       else
         score_tiles_kernel<<<score_grid, P, score_smem, stream>>>(g);
@@ -1513,8 +1597,12 @@ void Engine::loop_score_all(double* smice, std::uint8_t* feasible, double* max_e
   const long long C = (long long)I.cs.size();
   I.upload_iteration(0, C);
   I.launch_score(C);
-  std::vector<double> ps(size_t(C) * I.L), pm(size_t(C) * I.L), pc(static_cast<size_t>(C));
-  const bool mag = I.cfg.objective == Objective::magnitude;
+  // score3 writes scenario-major [L][ldc]; the complex scorer candidate-major [C][L]
+  const bool tr = I.cfg.objective == Objective::magnitude && I.use_score3;
+  const size_t ldc = size_t(I.s3_ldc());
+  const size_t npair = tr ? ldc * I.L : size_t(C) * I.L;
+  std::vector<double> ps(npair), pm(npair), pc(static_cast<size_t>(C));
+  const bool mag = I.cfg.objective == Objective::magnitude && !I.use_score3;
   if (C > 0) {
     if (mag)
       CK(cudaMemcpyAsync(pc.data(), I.d_pcand.p, pc.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
@@ -1532,9 +1620,10 @@ void Engine::loop_score_all(double* smice, std::uint8_t* feasible, double* max_e
     bool feas = true;
     double sum = 0;
     for (int l = 0; l < I.L; ++l) {
-      feas = feas && !(pm[size_t(c) * I.L + l] > I.cfg.e_bar);
-      sum += ps[size_t(c) * I.L + l];
-      if (max_err) max_err[size_t(c) * I.L + l] = pm[size_t(c) * I.L + l];
+      const size_t o = tr ? size_t(l) * ldc + size_t(c) : size_t(c) * I.L + l;
+      feas = feas && !(pm[o] > I.cfg.e_bar);
+      sum += ps[o];
+      if (max_err) max_err[size_t(c) * I.L + l] = pm[o];
     }
     feasible[c] = feas ? 1 : 0;
     smice[c] = feas ? sum : std::numeric_limits<double>::infinity();

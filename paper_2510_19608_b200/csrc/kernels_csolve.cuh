@@ -469,13 +469,27 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   for (int fr = 0; fr < a.nfr; ++fr) {
     const int4 nx = fs[(fr + 1) * 32 + lane];
     const int4 nxx = fx[(fr + 1) * 32 + lane];
-    if (rc.x >= 0 && rx.x == 0) {
+    if (rc.x >= 0 && rc.z >= 0) {
+      // scalar step: two pulls inline (zero pulls when absent), their
+      // products in flight together; the subtractions keep elimination order
       const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y);
-      C2 b = dev::csub(b0, dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj)));
+      const C2 t1 = lds2(xs + rx.x), a1 = lds2(cs + rx.y);
+      const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
+      const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
+      C2 b = dev::csub(dev::csub(b0, u0), u1);
+      int e = rx.z;
+      const int e_end = rx.z + rx.w;
 #pragma unroll 1
-      for (int e = rx.z; e < rx.z + rx.w; ++e) {
-        const int2 en = fe[e];
-        b = dev::csub(b, dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16))));
+      for (; e < e_end; e += 3) {  // further children, predicated batches of three
+        C2 u[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int2 en = fe[min(e + q, e_end - 1)];
+          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (e + q < e_end) b = dev::csub(b, u[q]);
       }
       sts2(xs + rc.x, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, b)));
     } else if (rc.x >= 0) {
@@ -525,10 +539,19 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     if (rc.x >= 0 && rx.x == 0) {
       const C2 xj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y), t = lds2(xs + rc.x);
       C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj)));
+      int e = rx.z;
+      const int e_end = rx.z + rx.w;
 #pragma unroll 1
-      for (int e = rx.z; e < rx.z + rx.w; ++e) {
-        const int2 en = be[e];
-        acc = dev::cadd(acc, dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16))));
+      for (; e < e_end; e += 3) {  // predicated batches of three
+        C2 u[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int2 en = be[min(e + q, e_end - 1)];
+          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (e + q < e_end) acc = dev::cadd(acc, u[q]);
       }
       sts2(xs + rc.x, dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc))));
     } else if (rc.x >= 0) {

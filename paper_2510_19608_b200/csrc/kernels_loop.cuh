@@ -30,6 +30,11 @@ namespace {
 struct LoopArgs {
   LoopState* st;
   int n, nb, slack, L, nphi, G, cap;
+  int cpc[4];          // candidates per scorer CTA for each |phi(r)| group (1..3)
+  int nsl;             // scenario slices per candidate group (score3), 1 otherwise
+  const double* psm;   // score3 per-pair SMICE [L][ldc] (null: pcand holds per-candidate sums)
+  int ldc;
+  double e_bar;
   int has_target;
   double target;
   const int* br_from;
@@ -249,9 +254,9 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     st->grp_start[2] = cnt1;
     st->grp_start[3] = cnt1 + cnt2;
     st->grp_cta[0] = 0;
-    st->grp_cta[1] = (cnt1 + a.G - 1) / a.G;
-    st->grp_cta[2] = st->grp_cta[1] + (cnt2 + a.G - 1) / a.G;
-    st->grp_cta[3] = st->grp_cta[2] + (cnt3 + a.G - 1) / a.G;
+    st->grp_cta[1] = (cnt1 + a.cpc[1] - 1) / a.cpc[1] * a.nsl;
+    st->grp_cta[2] = st->grp_cta[1] + (cnt2 + a.cpc[2] - 1) / a.cpc[2] * a.nsl;
+    st->grp_cta[3] = st->grp_cta[2] + (cnt3 + a.cpc[3] - 1) / a.cpc[3] * a.nsl;
     if (a.use_cond) cudaGraphSetConditional(a.cond, 1u);
     if (a.tdbg) a.tdbg[size_t(st->iter) * 8 + 3] = globaltimer();
   }
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   double bs = __longlong_as_double(0x7ff0000000000000LL);
   int bi = -1;
   for (int c = tid; c < C; c += kLoopThreads) {
-    const double v = a.pcand[c];
+    const double v = a.psm ? s3_candidate(a.psm, a.pmaxerr, c, a.L, a.ldc, a.e_bar) : a.pcand[c];
     if (!(v < 0.0) && loop_better(v, c, bs, bi)) {
       bs = v;
       bi = c;
@@ -328,7 +333,8 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
       a.tr_smice[it] = bs;
       a.tr_t[it] = globaltimer();
     }
-    for (int l = tid; l < L; l += kLoopThreads) a.tr_me[size_t(it) * L + l] = a.pmaxerr[size_t(bi) * L + l];
+    for (int l = tid; l < L; l += kLoopThreads)
+      a.tr_me[size_t(it) * L + l] = a.ldc > 0 ? a.pmaxerr[size_t(l) * a.ldc + bi] : a.pmaxerr[size_t(bi) * L + l];
   }
   // i_agg[s] += i_agg[r], i_agg[r] = 0 (reduce.cpp:336-343); bounds merge
   const unsigned ms = a.mask[s], mr = a.mask[r];

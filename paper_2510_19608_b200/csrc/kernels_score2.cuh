@@ -41,6 +41,59 @@ struct Score2Layout {
   }
 };
 
+// NR plain rows (single-row super-nodes, not the candidate's s or r): Vc,
+// |Vc|, the exact cluster error, then NR super-node boundaries of the ordered
+// fold. All NR rows are independent until the fold (ILP NR).
+template <int NL, int NR>
+__device__ __forceinline__ void score2_plain(const double2* __restrict__ bvp, const double2* __restrict__ zp, int L2,
+                                             int u0, const C2 (&cv)[NL], double& smice, double& cm, double& mx) {
+  double em[NR];
+  bool bad = false;
+#pragma unroll
+  for (int v = 0; v < NR; ++v) {
+    const double2 b0 = bvp[(u0 + v) * L2], b1 = bvp[(u0 + v) * L2 + 1];
+    double vx = b0.x, vy = b0.y;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const double2 dz = zp[(k * 2) * K2 + u0 + v];
+      vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
+      vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
+    }
+    const double s2 = dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy));
+    bad = bad || !sqrt_fast_ok(s2);
+    const double m = sqrt_rn_fast(s2);
+    em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
+  }
+  if (__any_sync(0xffffffffu, bad)) {  // |Vc|^2 outside the fast sqrt range: exact path
+#pragma unroll
+    for (int v = 0; v < NR; ++v) {
+      const double2 b0 = bvp[(u0 + v) * L2], b1 = bvp[(u0 + v) * L2 + 1];
+      double vx = b0.x, vy = b0.y;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        const double2 dz = zp[(k * 2) * K2 + u0 + v];
+        vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
+        vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
+      }
+      const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
+      em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
+    }
+  }
+  // NR super-node boundaries (reduce.cpp:110-121): close the open cluster;
+  // the row's error is the new cluster's maximum
+#pragma unroll
+  for (int v = 0; v < NR; ++v) {
+    smice = dev::dadd(smice, cm);
+    cm = em[v];
+    mx = dmax(mx, em[v]);
+  }
+}
+
+__device__ __forceinline__ bool score2_block_plain(uint4 e4) {
+  return ((e4.x & e4.y & e4.z & e4.w) & 4u) && ((e4.x & 3u) != 3u) && ((e4.y & 3u) != 3u) && ((e4.z & 3u) != 3u) &&
+         ((e4.w & 3u) != 3u);
+}
+
 template <int NL>
 __device__ __forceinline__ void score2_body(const RowArgs& a, int cta, int g_begin, int g_count, int R,
                                             double* smd) {
@@ -96,17 +149,28 @@ __device__ __forceinline__ void score2_body(const RowArgs& a, int cta, int g_beg
   const size_t nphi = size_t(a.nphi);
   const int ntiles = (R + K2 - 1) / K2;
 
+  // each thread stages a fixed 16-byte column of every bv row it owns when
+  // the CTA width is a multiple of a row's 2L chunks (no divisions per chunk)
+  const bool bv_fixed = (P % (2 * L)) == 0;
+  const int bv_rem = tid % (2 * L), bv_u0 = tid / (2 * L), bv_du = P / (2 * L);
   auto stage = [&](int j, int b) {
     const int t0 = j * K2;
     for (int i = tid; i < K2 / 4; i += P) cp_async16(tab_s(b) + 4 * i, a.tab + t0 + 4 * i);
     // (base, bounds): global [rho][L][2] -> shared [row][L][2] (consecutive
     // scenarios contiguous: conflict-free 16-byte reads across a warp)
-    const int nbv = K2 * L * 2;
-    for (int i = tid; i < nbv; i += P) {
-      const int u = i / (2 * L);
-      const int rem = i - u * 2 * L;
-      const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-      cp_async16(bv_s(b) + size_t(u) * 2 * L + rem, a.bv + rho * 2 * L + rem);
+    if (bv_fixed) {
+      for (int u = bv_u0; u < K2; u += bv_du) {
+        const size_t rho = __ldg(a.tab + t0 + u) >> 3;
+        cp_async16(bv_s(b) + size_t(u) * 2 * L + bv_rem, a.bv + rho * 2 * L + bv_rem);
+      }
+    } else {
+      const int nbv = K2 * L * 2;
+      for (int i = tid; i < nbv; i += P) {
+        const int u = i / (2 * L);
+        const int rem = i - u * 2 * L;
+        const size_t rho = __ldg(a.tab + t0 + u) >> 3;
+        cp_async16(bv_s(b) + size_t(u) * 2 * L + rem, a.bv + rho * 2 * L + rem);
+      }
     }
     // Zs / Zr rows of the CTA's candidates: shared [g][k][2][row]
     const int nz = G * NL * 2 * K2;
@@ -147,58 +211,25 @@ __device__ __forceinline__ void score2_body(const RowArgs& a, int cta, int g_beg
     const unsigned* tb = tab_s(b);
     const double2* bvp = bv_s(b) + size_t(l) * 2;  // this thread's scenario, row stride 2L
     const double2* zp = z_s(b) + size_t(gl) * NL * 2 * K2;
+    int q = 0;
 #pragma unroll 1
-    for (int q = 0; q < K2 / 4; ++q) {
+    while (q < K2 / 4) {
       const int blk = (t0 >> 2) + q;
       const uint4 e4 = *reinterpret_cast<const uint4*>(tb + 4 * q);
-      const unsigned e[4] = {e4.x, e4.y, e4.z, e4.w};
-      // four single-row super-nodes, no padding: every entry has the first bit
-      // and a real phase; the phases differ from 3
-      const bool plain = ((e4.x & e4.y & e4.z & e4.w) & 4u) && ((e4.x & 3u) != 3u) && ((e4.y & 3u) != 3u) &&
-                         ((e4.z & 3u) != 3u) && ((e4.w & 3u) != 3u);
-      const bool mine = blk == sblk || blk == rblk;
+      const bool fast = score2_block_plain(e4) && !__any_sync(0xffffffffu, blk == sblk || blk == rblk);
+      if (fast && q + 1 < K2 / 4) {
+        const uint4 f4 = *reinterpret_cast<const uint4*>(tb + 4 * q + 4);
+        if (score2_block_plain(f4) && !__any_sync(0xffffffffu, blk + 1 == sblk || blk + 1 == rblk)) {
+          score2_plain<NL, 8>(bvp, zp, L2, 4 * q, cv, smice, cm, mx);
+          q += 2;
+          continue;
+        }
+      }
       const int u0 = 4 * q;
+      const unsigned e[4] = {e4.x, e4.y, e4.z, e4.w};
       double em[4];
-      bool bad = false;
-      if (plain && !__any_sync(0xffffffffu, mine)) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const double2 b0 = bvp[(u0 + v) * L2], b1 = bvp[(u0 + v) * L2 + 1];
-          double vx = b0.x, vy = b0.y;
-#pragma unroll
-          for (int k = 0; k < NL; ++k) {
-            const double2 dz = zp[(k * 2) * K2 + u0 + v];
-            vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
-            vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
-          }
-          const double s2 = dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy));
-          bad = bad || !sqrt_fast_ok(s2);
-          const double m = sqrt_rn_fast(s2);
-          em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
-        }
-        if (__any_sync(0xffffffffu, bad)) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const double2 b0 = bvp[(u0 + v) * L2], b1 = bvp[(u0 + v) * L2 + 1];
-            double vx = b0.x, vy = b0.y;
-#pragma unroll
-            for (int k = 0; k < NL; ++k) {
-              const double2 dz = zp[(k * 2) * K2 + u0 + v];
-              vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
-              vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
-            }
-            const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
-            em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
-          }
-        }
-        // four super-node boundaries (reduce.cpp:110-121): close the open
-        // cluster, the row's error is the new cluster's maximum
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          smice = dev::dadd(smice, cm);
-          cm = em[v];
-          mx = dmax(mx, em[v]);
-        }
+      if (fast) {
+        score2_plain<NL, 4>(bvp, zp, L2, u0, cv, smice, cm, mx);
       } else {
         // general block: padding, multi-row super-nodes, the candidate's s
         // (bounds merged with r's, reduce.cpp:114-115) and r (skipped, :111)
@@ -231,6 +262,7 @@ __device__ __forceinline__ void score2_body(const RowArgs& a, int cta, int g_beg
           mx = dmax(mx, em[v]);
         }
       }
+      ++q;
     }
   }
   smice = dev::dadd(smice, cm);

@@ -1,0 +1,432 @@
+// score3: the production magnitude-objective scorer (reduce.cpp:89-123,
+// 194-244). One thread per (candidate, scenario) pair.
+//
+// A CTA owns Gk candidates x Ls scenarios (a scenario slice; Gk = G / |phi(r)|
+// so the staged Z columns always fit G slots) and walks the iteration's row
+// table in tiles of K3 = 16 rows (four 4-row blocks; a block never splits a
+// super-node). Tiles stream through a three-slot shared-memory ring with one
+// barrier per tile:
+//
+//   iteration j:  wait for tile j+1's cp.async group -> __syncthreads ->
+//                 issue tile j+2 into the slot tile j-1 used ->
+//                 form D = Zs - Zr of tile j+1 in place (once per candidate and
+//                 phase, shared by the slice's scenarios) -> compute tile j.
+//
+// The scenario slice keeps the (base, bounds) tile small and independent of
+// L, so occupancy does not fall as the scenario count grows. Each pair writes
+// its SMICE and max_err; the scenario sum in scenario order and the
+// feasibility test (reduce.cpp:221-242) run in the argmin/commit kernel.
+//
+// Per 4-row block the common case (single-row super-nodes, none of them the
+// candidate's s or r, no padding) runs straight-line code over 8 or 4 rows:
+// Vc = base + sum_p c_p D_p, |Vc| (branch-free correctly rounded sqrt),
+// em = max(m - min_j v_j, max_j v_j - m) (exact cluster maximum), the ordered
+// SMICE sum and the running max_err. Other blocks take the general per-row
+// path; a block whose |Vc|^2 leaves the fast sqrt range is redone with
+// __dsqrt_rn.
+#pragma once
+
+namespace kronred::b200 {
+namespace {
+
+constexpr int K3 = 16;  // rows per tile
+
+struct S3Args {
+  int C, L, nphi, R;
+  int G;                     // Z column slots per CTA (candidates per CTA = G / |phi(r)|)
+  int Ls, nsl;               // scenario slice width and slice count
+  const int4* cand;          // grouped by |phi(r)|: (s, r, table row of s, table row of r)
+  const int* cand_idx;       // lexicographic index of each grouped slot
+  const unsigned* tab;       // (rho << 3) | (first << 2) | phase, padded
+  const std::uint8_t* mask;
+  const int* prow_off;
+  const double2* Z;          // [nphi cols][nphi rows]
+  const double2* bv;         // [rho][L][2]
+  const double2* iagg;       // [n][L][3]
+  double* out_sm;            // [L][ldc] per-pair SMICE (lexicographic candidate index)
+  double* out_mx;            // [L][ldc] per-pair max_err
+  int ldc;                   // leading dimension (>= largest candidate count)
+  double e_bar;
+  double* out_cand;          // [C] per-candidate SMICE (scenario order) or -1 (infeasible)
+  int* grp_done;             // [candidate groups] slice-completion counters (zeroed, self-resetting)
+  int grp_start[4];          // candidate offset of each |phi(r)| group (1..3)
+  int grp_cta[4];            // first CTA of each group; grp_cta[3] = CTAs in use
+  const LoopState* st;       // device-resident loop: C, R and the layout come from here
+  unsigned long long* tdbg;
+};
+
+struct S3Layout {
+  int Ls, G;
+  __host__ __device__ size_t tab_e() const { return (K3 * 4 + 15) / 16; }  // double2 units
+  __host__ __device__ size_t bv_e() const { return size_t(Ls) * K3 * 2; }
+  __host__ __device__ size_t z_e() const { return size_t(G) * 2 * K3; }    // Zs and Zr staging
+  __host__ __device__ size_t buf_e() const { return tab_e() + bv_e() + z_e(); }
+  __host__ __device__ size_t smem_bytes() const { return 3 * buf_e() * sizeof(double2) + size_t(G) * 2 * sizeof(int) + 64; }
+};
+
+// NR plain rows: Vc, |Vc|, exact cluster error, then NR super-node
+// boundaries of the ordered fold (ILP NR until the fold).
+template <int NL, int NR>
+__device__ __forceinline__ void s3_plain(const double2* __restrict__ bvp, const double2* __restrict__ zp, int RS,
+                                         int u0, const C2 (&cv)[NL], double& smice, double& cm, double& mx) {
+  double em[NR];
+  bool bad = false;
+#pragma unroll
+  for (int v = 0; v < NR; ++v) {
+    const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+    double vx = b0.x, vy = b0.y;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const double2 dz = zp[(k * 2) * K3 + u0 + v];
+      vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
+      vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
+    }
+    const double s2 = dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy));
+    bad = bad || !sqrt_fast_ok(s2);
+    const double m = sqrt_rn_fast(s2);
+    em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+    for (int v = 0; v < NR; ++v) {
+      const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+      double vx = b0.x, vy = b0.y;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        const double2 dz = zp[(k * 2) * K3 + u0 + v];
+        vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
+        vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
+      }
+      const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
+      em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NR; ++v) {
+    smice = dev::dadd(smice, cm);
+    cm = em[v];
+    mx = dmax(mx, em[v]);
+  }
+}
+
+__device__ __forceinline__ bool s3_block_plain(uint4 e4) {
+  return ((e4.x & e4.y & e4.z & e4.w) & 4u) && ((e4.x & 3u) != 3u) && ((e4.y & 3u) != 3u) && ((e4.z & 3u) != 3u) &&
+         ((e4.w & 3u) != 3u);
+}
+
+// Per-candidate scenario reduction of score3's per-pair results: SMICE summed
+// in scenario order ((0 + s_0) + s_1) + ... (reduce.cpp:221-242), feasible
+// iff every scenario's max_err <= e_bar.
+__device__ __forceinline__ double s3_candidate(const double* sm, const double* mxv, int c, int L, int ldc,
+                                               double e_bar) {
+  double sum = 0.0;
+  bool feasible = true;
+  for (int l0 = 0; l0 < L; l0 += 8) {
+    double v[8], m[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // issue the slice's loads together, then the ordered adds
+      const bool in = l0 + u < L;
+      v[u] = in ? __ldcg(sm + size_t(l0 + u) * ldc + c) : 0.0;  // L2: written by other CTAs
+      m[u] = in ? __ldcg(mxv + size_t(l0 + u) * ldc + c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (l0 + u < L) {
+        sum = dev::dadd(sum, v[u]);
+        feasible = feasible && !(m[u] > e_bar);
+      }
+  }
+  return feasible ? sum : -1.0;  // a feasible SMICE is never negative
+}
+
+template <int NL>
+__device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin, int g_count, int R, double* smd,
+                                        int g_base_group) {
+  const int L = a.L, Ls = a.Ls;
+  const int Gk = a.G / NL;
+  const int P = blockDim.x;
+  const int tid = threadIdx.x;
+  const int cgrp = local / a.nsl, sl = local - cgrp * a.nsl;
+  const int gl = min(tid / Ls, Gk - 1);
+  const int ll = tid - (tid / Ls) * Ls;
+  const int l = min(sl * Ls + ll, L - 1);
+  const int cg = cgrp * Gk + gl;
+  const bool valid = tid < Gk * Ls && cg < g_count && sl * Ls + ll < L;
+  const int c = g_begin + min(cg, g_count - 1);
+  const S3Layout lay{Ls, a.G};
+  double2* base2 = reinterpret_cast<double2*>(smd);
+  const size_t buf_e = lay.buf_e();
+  auto tab_s = [&](int b) { return reinterpret_cast<unsigned*>(base2 + b * buf_e); };
+  auto bv_s = [&](int b) { return base2 + b * buf_e + lay.tab_e(); };
+  auto z_s = [&](int b) { return base2 + b * buf_e + lay.tab_e() + lay.bv_e(); };
+  int* zcol = reinterpret_cast<int*>(base2 + 3 * buf_e);  // [Gk][NL][2]
+
+  const int4 cd = a.cand[c];
+  const int s = cd.x, r = cd.y;
+  const int ts0 = cd.z, tr0 = cd.w;
+  const int sblk = ts0 >> 2, rblk = tr0 >> 2;  // a super-node's rows share one 4-row block
+  const unsigned ms = a.mask[s], mr = a.mask[r];
+  const int ts1 = ts0 + __popc(ms), tr1 = tr0 + NL;
+  const int rs0 = a.prow_off[s], rr0 = a.prow_off[r];
+  const double INF = __longlong_as_double(0x7ff0000000000000LL);
+  C2 cv[NL];
+  double rlo0 = INF, rlo1 = INF, rlo2 = INF, rhi0 = -INF, rhi1 = -INF, rhi2 = -INF;
+  {
+    int j = 0;
+#pragma unroll
+    for (int ph = 0; ph < 3; ++ph) {
+      if (!((mr >> ph) & 1u)) continue;
+      const int rr = rr0 + popc_below(mr, ph);
+      const double2 bnd = a.bv[(size_t(rr) * L + l) * 2 + 1];
+      if (ph == 0) { rlo0 = bnd.x; rhi0 = bnd.y; }
+      if (ph == 1) { rlo1 = bnd.x; rhi1 = bnd.y; }
+      if (ph == 2) { rlo2 = bnd.x; rhi2 = bnd.y; }
+      const C2 cz = ld2(a.iagg + (size_t(r) * L + l) * 3 + ph);
+#pragma unroll
+      for (int k = 0; k < NL; ++k)
+        if (k == j) cv[k] = cz;
+      if (ll == 0 && tid < Gk * Ls) {
+        zcol[(gl * NL + j) * 2 + 0] = rs0 + popc_below(ms, ph);
+        zcol[(gl * NL + j) * 2 + 1] = rr;
+      }
+      ++j;
+    }
+  }
+  __syncthreads();
+  const size_t nphi = size_t(a.nphi);
+  const int ntiles = (R + K3 - 1) / K3;
+  // (base, bounds) slice staging: each row is 2*Ls contiguous 16-byte chunks
+  const int RS = 2 * Ls;
+  const int nsc = min(Ls, L - sl * Ls);  // scenarios of this slice
+  const bool bv_fixed = (P % RS) == 0;
+  const int bv_ch = tid % RS, bv_u0 = tid / RS, bv_du = P / RS;
+  const size_t bv_off = size_t(sl) * Ls * 2;
+
+  auto stage = [&](int j, int b) {
+    const int t0 = j * K3;
+    for (int i = tid; i < K3 / 4; i += P) cp_async16(tab_s(b) + 4 * i, a.tab + t0 + 4 * i);
+    if (bv_fixed) {
+      if (bv_ch < 2 * nsc)
+        for (int u = bv_u0; u < K3; u += bv_du) {
+          const size_t rho = __ldg(a.tab + t0 + u) >> 3;
+          cp_async16(bv_s(b) + size_t(u) * RS + bv_ch, a.bv + rho * 2 * L + bv_off + bv_ch);
+        }
+    } else {
+      for (int i = tid; i < K3 * RS; i += P) {
+        const int u = i / RS, ch = i - u * RS;
+        if (ch >= 2 * nsc) continue;
+        const size_t rho = __ldg(a.tab + t0 + u) >> 3;
+        cp_async16(bv_s(b) + size_t(u) * RS + ch, a.bv + rho * 2 * L + bv_off + ch);
+      }
+    }
+    const int nz = Gk * NL * 2 * K3;
+    for (int i = tid; i < nz; i += P) {
+      const int u = i % K3;
+      const int col = zcol[i / K3];
+      const size_t rho = __ldg(a.tab + t0 + u) >> 3;
+      cp_async16(z_s(b) + i, a.Z + size_t(col) * nphi + rho);
+    }
+  };
+  // Fast staging: each thread owns at most two bv rows and one Z row of every
+  // tile, so the table entries it needs are prefetched into registers one
+  // tile ahead (no dependent global load in front of each cp.async).
+  const bool fst = bv_fixed && (P % K3) == 0 && 2 * bv_du >= K3;
+  const int u_a = bv_u0, u_b = bv_u0 + bv_du, u_z = tid % K3;
+  auto load_rho = [&](int j, unsigned (&rr)[3]) {
+    const int t0 = j * K3;
+    rr[0] = (j < ntiles && u_a < K3) ? __ldg(a.tab + t0 + u_a) >> 3 : 0u;
+    rr[1] = (j < ntiles && u_b < K3) ? __ldg(a.tab + t0 + u_b) >> 3 : 0u;
+    rr[2] = j < ntiles ? __ldg(a.tab + t0 + u_z) >> 3 : 0u;
+  };
+  auto stage_fast = [&](int j, int b, const unsigned (&rr)[3]) {
+    const int t0 = j * K3;
+    if (tid < K3 / 4) cp_async16(tab_s(b) + 4 * tid, a.tab + t0 + 4 * tid);
+    if (bv_ch < 2 * nsc) {
+      if (u_a < K3) cp_async16(bv_s(b) + size_t(u_a) * RS + bv_ch, a.bv + size_t(rr[0]) * 2 * L + bv_off + bv_ch);
+      if (u_b < K3) cp_async16(bv_s(b) + size_t(u_b) * RS + bv_ch, a.bv + size_t(rr[1]) * 2 * L + bv_off + bv_ch);
+    }
+    const int nz = Gk * NL * 2 * K3;
+    for (int i = tid; i < nz; i += P) cp_async16(z_s(b) + i, a.Z + size_t(zcol[i / K3]) * nphi + rr[2]);
+  };
+  auto form_d = [&](int b) {  // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row)
+    double2* zz = z_s(b);
+    const int nd = Gk * NL * K3;
+    for (int i = tid; i < nd; i += P) {
+      const int col2 = i / K3, u = i - col2 * K3;
+      const double2 za = zz[(col2 * 2 + 0) * K3 + u], zr = zz[(col2 * 2 + 1) * K3 + u];
+      zz[(col2 * 2 + 0) * K3 + u] = make_double2(dev::dsub(za.x, zr.x), dev::dsub(za.y, zr.y));
+    }
+  };
+
+  double smice = 0.0, mx = 0.0, cm = 0.0;
+  unsigned rn[3];
+  if (fst) {
+    unsigned r0[3], r1[3];
+    load_rho(0, r0);
+    load_rho(1, r1);
+    stage_fast(0, 0, r0);
+    cp_async_commit();
+    if (ntiles > 1) stage_fast(1, 1, r1);
+    cp_async_commit();
+    load_rho(2, rn);
+  } else {
+    stage(0, 0);
+    cp_async_commit();
+    if (ntiles > 1) stage(1, 1);
+    cp_async_commit();
+  }
+  cp_async_wait1();
+  __syncthreads();
+  form_d(0);
+  for (int j = 0; j < ntiles; ++j) {
+    const int b = j % 3;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    if (fst) {
+      if (j + 2 < ntiles) stage_fast(j + 2, (j + 2) % 3, rn);
+      cp_async_commit();
+      load_rho(j + 3, rn);  // consumed next iteration: latency hidden by this tile's compute
+    } else {
+      if (j + 2 < ntiles) stage(j + 2, (j + 2) % 3);
+      cp_async_commit();
+    }
+    if (j + 1 < ntiles) form_d((j + 1) % 3);
+    const int t0 = j * K3;
+    const unsigned* tb = tab_s(b);
+    const double2* bvp = bv_s(b) + size_t(ll) * 2;  // this thread's scenario, row stride 2*Ls
+    const double2* zp = z_s(b) + size_t(gl) * NL * 2 * K3;
+    int q = 0;
+#pragma unroll 1
+    while (q < K3 / 4) {
+      const int blk = (t0 >> 2) + q;
+      const uint4 e4 = *reinterpret_cast<const uint4*>(tb + 4 * q);
+      const bool fast = s3_block_plain(e4) && !__any_sync(0xffffffffu, blk == sblk || blk == rblk);
+      if (fast && q + 1 < K3 / 4) {
+        const uint4 f4 = *reinterpret_cast<const uint4*>(tb + 4 * q + 4);
+        if (s3_block_plain(f4) && !__any_sync(0xffffffffu, blk + 1 == sblk || blk + 1 == rblk)) {
+          s3_plain<NL, 8>(bvp, zp, RS, 4 * q, cv, smice, cm, mx);
+          q += 2;
+          continue;
+        }
+      }
+      if (fast) {
+        s3_plain<NL, 4>(bvp, zp, RS, 4 * q, cv, smice, cm, mx);
+      } else {
+        // general block: padding, multi-row super-nodes, the candidate's s
+        // (bounds merged with r's, reduce.cpp:114-115) and r (skipped, :111)
+        const int u0 = 4 * q;
+        const unsigned e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int t = t0 + u0 + v;
+          const unsigned ev = e[v];
+          const unsigned ph = ev & 3u;
+          const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+          double vx = b0.x, vy = b0.y;
+#pragma unroll
+          for (int k = 0; k < NL; ++k) {
+            if (dev::cis0(cv[k])) continue;  // reduce.cpp:227: a zero current adds nothing
+            const double2 dz = zp[(k * 2) * K3 + u0 + v];
+            vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
+            vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
+          }
+          const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
+          double lo = b1.x, hi = b1.y;
+          if (t >= ts0 && t < ts1 && ph != 3u) {
+            lo = dmin(lo, ph == 0u ? rlo0 : (ph == 1u ? rlo1 : rlo2));
+            hi = dmax(hi, ph == 0u ? rhi0 : (ph == 1u ? rhi1 : rhi2));
+          }
+          const double e_v = ((t >= tr0 && t < tr1) || ph == 3u) ? 0.0 : dmax(dev::dsub(m, lo), dev::dsub(hi, m));
+          if (ev & 4u) {
+            smice = dev::dadd(smice, cm);
+            cm = 0.0;
+          }
+          cm = dmax(cm, e_v);
+          mx = dmax(mx, e_v);
+        }
+      }
+      ++q;
+    }
+  }
+  smice = dev::dadd(smice, cm);
+  if (valid) {
+    const size_t o = size_t(l) * a.ldc + a.cand_idx[c];
+    a.out_sm[o] = smice;
+    a.out_mx[o] = mx;
+  }
+  // the last slice CTA of a candidate group reduces its candidates over the
+  // scenarios (threadfence reduction: counters reset themselves)
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  const int grp = (local / a.nsl) + g_base_group;
+  if (tid == 0) {
+    const int old = atomicAdd(a.grp_done + grp, 1);
+    s_last = old == a.nsl - 1;
+    if (s_last) a.grp_done[grp] = 0;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    // stage the group's per-pair results in shared memory (all threads, L2
+    // reads), then one thread per candidate sums in scenario order
+    double* ssm = smd;                       // [Gk][L]
+    double* smx = smd + size_t(Gk) * L;      // [Gk][L]
+    for (int i = tid; i < Gk * L; i += P) {
+      const int g = i / L, ls = i - g * L;
+      const int cgc = cgrp * Gk + g;
+      if (cgc < g_count) {
+        const size_t o = size_t(ls) * a.ldc + a.cand_idx[g_begin + cgc];
+        ssm[i] = __ldcg(a.out_sm + o);  // written by other CTAs: read through L2
+        smx[i] = __ldcg(a.out_mx + o);
+      }
+    }
+    __syncthreads();
+    const int cgc = cgrp * Gk + tid;
+    if (tid < Gk && cgc < g_count) {
+      double sum = 0.0;
+      bool feasible = true;
+      for (int ls = 0; ls < L; ++ls) {  // ((0 + s_0) + s_1) + ... (reduce.cpp:221-242)
+        sum = dev::dadd(sum, ssm[tid * L + ls]);
+        feasible = feasible && !(smx[tid * L + ls] > a.e_bar);
+      }
+      a.out_cand[a.cand_idx[g_begin + cgc]] = feasible ? sum : -1.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) score3_kernel(S3Args a) {
+  extern __shared__ double sm_dyn[];
+  const int b = blockIdx.x;
+  int C = a.C, R = a.R;
+  const int* gs = a.grp_start;
+  const int* gc = a.grp_cta;
+  if (a.st) {
+    if (a.st->done) return;
+    if (a.tdbg && b == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      a.tdbg[size_t(a.st->iter) * 8 + 6] = t;
+    }
+    C = a.st->C;
+    R = a.st->R;
+    gs = a.st->grp_start;
+    gc = a.st->grp_cta;
+  }
+  // work items (candidate group x scenario slice) strided over the grid: the
+  // device loop launches a fixed, occupancy-sized grid for every iteration
+  for (int w = b; w < gc[3]; w += gridDim.x) {
+    // counter slot: global candidate-group index (every group range is a
+    // whole number of nsl-slice items)
+    if (w < gc[1])
+      s3_body<1>(a, w, gs[1], gs[2] - gs[1], R, sm_dyn, 0);
+    else if (w < gc[2])
+      s3_body<2>(a, w - gc[1], gs[2], gs[3] - gs[2], R, sm_dyn, gc[1] / a.nsl);
+    else
+      s3_body<3>(a, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
+    __syncthreads();  // shared memory is reused by the next item
+  }
+}
+
+}  // namespace
+}  // namespace kronred::b200
