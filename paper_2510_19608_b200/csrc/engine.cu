@@ -176,6 +176,9 @@ struct Engine::Impl {
   int grp_off[4] = {0, 0, 0, 0};
   std::vector<int> sn_pos;     // compact index of each active super-node
   DBuf<double> d_psmice, d_pmaxerr, d_pcand, d_best;
+  // final Kron / model-error solves reuse these (no cudaMalloc/cudaFree inside a run)
+  DevElim kron_e, merr_e;
+  DBuf<double2> merr_yin, merr_rhs, merr_out, merr_kv;
   DBuf<int> d_grpdone;  // score3 slice-completion counters
   bool use_tiles = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) != "rows";
   // score2 (kernels_score2.cuh) is the default; KRONRED_SCORER=tiles|seg|rows select the older variants
@@ -241,6 +244,12 @@ struct Engine::Impl {
   DBuf<unsigned long long> d_trt;
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the loop graph is instantiated once per engine and configuration
+  cudaGraph_t loop_graph = nullptr;
+  cudaGraphExec_t loop_exec = nullptr;
+  double loop_key_ebar = -1.0, loop_key_target = -1.0;
+  int loop_key_has = -1;
+  bool loop_key_trace = false;
   DBuf<unsigned long long> d_tdbg;
   bool loop_trace = std::getenv("KRONRED_LOOP_TRACE") != nullptr;
   bool force_host_loop = std::getenv("KRONRED_LOOP") != nullptr && std::string(std::getenv("KRONRED_LOOP")) == "host";
@@ -612,7 +621,9 @@ struct Engine::Impl {
 
   // K1f on the device: blocks <- input, fill <- 0, then the level executor,
   // then the present-phase compaction of the factor.
-  void factorize(DevElim& d, const double2* d_input, double floor) {
+  // check_now=false defers the singular-pivot check to check_deferred_fail()
+  // (no host round trip inside a run; the run's final sync reads the flag)
+  void factorize(DevElim& d, const double2* d_input, double floor, bool check_now = true) {
     const ElimSchedule& h = d.h;
     if (h.n_input > 0)
       CK(cudaMemcpyAsync(d.blocks.p, d_input, size_t(h.n_input) * 9 * sizeof(double2), cudaMemcpyDeviceToDevice,
@@ -648,9 +659,35 @@ struct Engine::Impl {
       launched();
       CK(cudaGetLastError());
     }
-    unsigned long long failed = 0;
-    CK(cudaMemcpyAsync(&failed, d.fail.p, sizeof(failed), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
+    if (!check_now) {
+      CK(cudaMemcpyAsync(h_fail, d.fail.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+      deferred_fail = &d;
+    } else {
+      unsigned long long failed = 0;
+      CK(cudaMemcpyAsync(&failed, d.fail.p, sizeof(failed), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      throw_if_failed(d, failed);
+    }
+    if (d.ncf_all > 0) {
+      compact_gather_kernel<<<(d.ncf_all + 255) / 256, 256, 0, stream>>>(d.ncf_all, d.gsrc.p, d.blocks.p,
+                                                                         d.pinv.p, d.cfac.p);
+      launched();
+      CK(cudaGetLastError());
+    }
+  }
+
+  unsigned long long* h_fail = nullptr;  // pinned
+  DevElim* deferred_fail = nullptr;
+  // after a stream sync: raise the SolverError a deferred factorization recorded
+  void check_deferred_fail() {
+    if (!deferred_fail) return;
+    DevElim* d = deferred_fail;
+    deferred_fail = nullptr;
+    throw_if_failed(*d, *h_fail);
+  }
+
+  void throw_if_failed(DevElim& d, unsigned long long failed) {
+    const ElimSchedule& h = d.h;
     if (failed != ~0ull) {
       double piv = 0;
       CK(cudaMemcpy(&piv, d.fail_pivot.p + failed, sizeof(double), cudaMemcpyDeviceToHost));
@@ -661,12 +698,6 @@ struct Engine::Impl {
                             " (smallest pivot " + buf + ", " + std::to_string(h.nsteps - int(failed)) + " of " +
                             std::to_string(h.nsteps) + " eliminations left)",
                         piv, node);
-    }
-    if (d.ncf_all > 0) {
-      compact_gather_kernel<<<(d.ncf_all + 255) / 256, 256, 0, stream>>>(d.ncf_all, d.gsrc.p, d.blocks.p,
-                                                                         d.pinv.p, d.cfac.p);
-      launched();
-      CK(cudaGetLastError());
     }
   }
 
@@ -753,6 +784,7 @@ struct Engine::Impl {
     if (device < 0) CK(cudaGetDevice(&device));
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&h_fail, sizeof(unsigned long long)));
     CK(cudaDeviceGetAttribute(&optin_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     for (auto fn : {csolve_kernel<CM_FULL>, csolve_kernel<CM_BASE>, csolve_kernel<CM_ZCOL>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
@@ -871,10 +903,15 @@ struct Engine::Impl {
       cudaEventDestroy(ev_run1);
     }
     if (h_best) cudaFreeHost(h_best);
+    if (h_fail) cudaFreeHost(h_fail);
+    if (h_loopst) cudaFreeHost(h_loopst);
+    if (h_trace) cudaFreeHost(h_trace);
     if (h_cand) cudaFreeHost(h_cand);
     if (h_snt) cudaFreeHost(h_snt);
     if (h_tab) cudaFreeHost(h_tab);
     if (h_cidx) cudaFreeHost(h_cidx);
+    if (loop_exec) cudaGraphExecDestroy(loop_exec);
+    if (loop_graph) cudaGraphDestroy(loop_graph);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
@@ -890,15 +927,12 @@ struct Engine::Impl {
     if (!c.use_delta) throw ConfigError("use_delta=false (naive per-candidate solves) is not implemented yet");
     cfg = c;
     // AnchoredSolver (re-factorized per run, as run_reduction does, reduce.cpp:359)
-    factorize(full, d_yin.p, pivot_floor);
+    factorize(full, d_yin.p, pivot_floor, /*check_now=*/false);
     solve_full(full, d_slackv.p, nullptr, 1, d_v0.p);
-    {
-      std::vector<double2> v0(size_t(3) * n);
-      CK(cudaMemcpyAsync(v0.data(), d_v0.p, v0.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      std::vector<double2> v0p(static_cast<size_t>(nphi));
-      for (int r = 0; r < nphi; ++r) v0p[size_t(r)] = v0[size_t(prow_node[size_t(r)]) * 3 + prow_phase[size_t(r)]];
-      CK(cudaMemcpyAsync(d_v0p.p, v0p.data(), v0p.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+    if (nphi > 0) {
+      gather_rows_kernel<<<(nphi + 255) / 256, 256, 0, stream>>>(nphi, d_prow_node.p, d_prow_phase.p, d_v0.p, d_v0p.p);
+      launched();
+      CK(cudaGetLastError());
     }
     const int tot = std::max(nphi * L, n * L * 3);
     prep_kernel<<<(tot + 255) / 256, 256, 0, stream>>>(n, L, nphi, d_prow_node.p, d_prow_phase.p, d_vhat.p, d_inj.p,
@@ -1288,8 +1322,8 @@ struct Engine::Impl {
       LoopState st0{};
       st0.done = target_reached() ? 1 : 0;
       st0.ns = n;
+      // pageable sources: cudaMemcpyAsync stages them before returning
       CK(cudaMemcpyAsync(d_loopst.p, &st0, sizeof st0, cudaMemcpyHostToDevice, stream));
-      CK(cudaStreamSynchronize(stream));  // host vectors go out of scope
     }
     LoopArgs la = loop_args();
     if (loop_trace) {
@@ -1338,10 +1372,13 @@ struct Engine::Impl {
     enum_kernel<<<1, kLoopThreads, enum_smem(), stream>>>(la);
     launched();
     CK(cudaGetLastError());
-    LoopState st{};
-    CK(cudaMemcpyAsync(&st, d_loopst.p, sizeof st, cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    if (!st.done) {
+    const bool key_ok = loop_exec && loop_key_ebar == cfg.e_bar && loop_key_has == la.has_target &&
+                        loop_key_target == la.target && loop_key_trace == loop_trace;
+    if (!key_ok) {
+      if (loop_exec) CK(cudaGraphExecDestroy(loop_exec));
+      if (loop_graph) CK(cudaGraphDestroy(loop_graph));
+      loop_exec = nullptr;
+      loop_graph = nullptr;
       cudaGraph_t graph;
       CK(cudaGraphCreate(&graph, 0));
       cudaGraphConditionalHandle h;
@@ -1382,16 +1419,37 @@ struct Engine::Impl {
       CK(cudaEventRecord(ev_join, stream2));
       CK(cudaStreamWaitEvent(stream, ev_join, 0));
       CK(cudaStreamEndCapture(stream, &body));
-      cudaGraphExec_t exec;
-      CK(cudaGraphInstantiate(&exec, graph, 0));
-      CK(cudaGraphLaunch(exec, stream));
-      CK(cudaStreamSynchronize(stream));
-      CK(cudaGraphExecDestroy(exec));
-      CK(cudaGraphDestroy(graph));
-      CK(cudaMemcpyAsync(&st, d_loopst.p, sizeof st, cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      launches += 4LL * (st.iter + 1);
+      CK(cudaGraphInstantiate(&loop_exec, graph, 0));
+      loop_graph = graph;
+      loop_key_ebar = cfg.e_bar;
+      loop_key_has = la.has_target;
+      loop_key_target = la.target;
+      loop_key_trace = loop_trace;
     }
+    // the whole loop: one graph launch (a loop that is already done runs one
+    // body of early-exit kernels); results come back with one sync
+    CK(cudaGraphLaunch(loop_exec, stream));
+    if (!h_loopst) {
+      CK(cudaMallocHost(&h_loopst, sizeof(LoopState)));
+      CK(cudaMallocHost(&h_trace, trace_bytes()));
+    }
+    CK(cudaMemcpyAsync(h_loopst, d_loopst.p, sizeof(LoopState), cudaMemcpyDeviceToHost, stream));
+    {
+      char* p = h_trace;
+      CK(cudaMemcpyAsync(p, d_trsr.p, sizeof(int) * 2 * size_t(n), cudaMemcpyDeviceToHost, stream));
+      p += sizeof(int) * 2 * size_t(n);
+      CK(cudaMemcpyAsync(p, d_trc.p, sizeof(int) * size_t(n), cudaMemcpyDeviceToHost, stream));
+      p += sizeof(int) * size_t(n);
+      CK(cudaMemcpyAsync(p, d_trsmice.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, stream));
+      p += sizeof(double) * size_t(n);
+      CK(cudaMemcpyAsync(p, d_trme.p, sizeof(double) * size_t(n) * L, cudaMemcpyDeviceToHost, stream));
+      p += sizeof(double) * size_t(n) * L;
+      CK(cudaMemcpyAsync(p, d_trt.p, sizeof(unsigned long long) * size_t(n), cudaMemcpyDeviceToHost, stream));
+    }
+    CK(cudaStreamSynchronize(stream));
+    check_deferred_fail();
+    const LoopState st = *h_loopst;
+    launches += 4LL * (st.iter + 1);
     const int it = st.iter;
     if (loop_trace && it > 2) {
       std::vector<unsigned long long> T(size_t(n + 1) * 8);
@@ -1424,21 +1482,29 @@ struct Engine::Impl {
     tr_me.resize(size_t(it) * L);
     tr_ms.assign(size_t(it), 0.0);
     if (it > 0) {
-      std::vector<int> sr(static_cast<size_t>(2 * it));
-      std::vector<unsigned long long> tt(static_cast<size_t>(it));
-      CK(cudaMemcpyAsync(sr.data(), d_trsr.p, sizeof(int) * sr.size(), cudaMemcpyDeviceToHost, stream));
-      CK(cudaMemcpyAsync(tr_c.data(), d_trc.p, sizeof(int) * size_t(it), cudaMemcpyDeviceToHost, stream));
-      CK(cudaMemcpyAsync(tr_smice.data(), d_trsmice.p, sizeof(double) * size_t(it), cudaMemcpyDeviceToHost, stream));
-      CK(cudaMemcpyAsync(tr_me.data(), d_trme.p, sizeof(double) * tr_me.size(), cudaMemcpyDeviceToHost, stream));
-      CK(cudaMemcpyAsync(tt.data(), d_trt.p, sizeof(unsigned long long) * size_t(it), cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
+      const char* p = h_trace;
+      const int* sr = reinterpret_cast<const int*>(p);
+      p += sizeof(int) * 2 * size_t(n);
+      std::memcpy(tr_c.data(), p, sizeof(int) * size_t(it));
+      p += sizeof(int) * size_t(n);
+      std::memcpy(tr_smice.data(), p, sizeof(double) * size_t(it));
+      p += sizeof(double) * size_t(n);
+      std::memcpy(tr_me.data(), p, sizeof(double) * size_t(it) * L);
+      p += sizeof(double) * size_t(n) * L;
+      const unsigned long long* tt = reinterpret_cast<const unsigned long long*>(p);
       for (int i = 0; i < it; ++i) {
-        tr_s[size_t(i)] = sr[size_t(2 * i)];
-        tr_r[size_t(i)] = sr[size_t(2 * i + 1)];
-        if (i > 0) tr_ms[size_t(i)] = double(tt[size_t(i)] - tt[size_t(i - 1)]) * 1e-6;
+        tr_s[size_t(i)] = sr[2 * i];
+        tr_r[size_t(i)] = sr[2 * i + 1];
+        if (i > 0) tr_ms[size_t(i)] = double(tt[i] - tt[i - 1]) * 1e-6;
       }
     }
   }
+
+  size_t trace_bytes() const {
+    return size_t(n) * (sizeof(int) * 3 + sizeof(double) * (1 + size_t(L)) + sizeof(unsigned long long));
+  }
+  LoopState* h_loopst = nullptr;
+  char* h_trace = nullptr;
 
   void commit_device(int s, int r) {
     const unsigned ms = prob.mask[size_t(s)], mr = prob.mask[size_t(r)];
@@ -1488,7 +1554,11 @@ void Engine::solve(const double* inj, int nrhs, double* out) {
   CK(cudaStreamSynchronize(I.stream));
 }
 
-void Engine::loop_begin(const ReductionConfig& cfg) { impl_->begin(cfg); }
+void Engine::loop_begin(const ReductionConfig& cfg) {
+  impl_->begin(cfg);
+  CK(cudaStreamSynchronize(impl_->stream));
+  impl_->check_deferred_fail();
+}
 
 void Engine::debug_base_refresh(int reps, double* ms, long long* clocks) {
   Impl& I = *impl_;
@@ -1682,6 +1752,10 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
   CK(cudaEventRecord(I.ev_run0, I.stream));
   I.begin(cfg);
   int iteration = 0;
+  if (!I.device_loop_ok(cfg)) {  // host-driven loop: surface a singular factorization first
+    CK(cudaStreamSynchronize(I.stream));
+    I.check_deferred_fail();
+  }
   if (I.device_loop_ok(cfg)) {
     // whole loop on the device; the host state machine replays the commits
     // afterwards to rebuild clusters and call the observer in order
@@ -1760,7 +1834,7 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
 
 void Engine::kron(const std::vector<int>& reduce, ReducedModel& model) {
   Impl& I = *impl_;
-  DevElim e;
+  DevElim& e = I.kron_e;
   I.upload_elim(e, I.prob.y, I.prob.mask, reduce, /*with_solve=*/false);
   I.factorize(e, I.d_yin.p, 1e-12 * std::max(I.prob.y.max_abs(), 1.0));
   const ElimSchedule& h = e.h;
@@ -1816,12 +1890,12 @@ std::vector<double> Engine::model_errors(const ReducedModel& model) {
   const FlatBlocks yk = FlatBlocks::from(model.y_kron);
   std::vector<std::uint8_t> kmask(static_cast<size_t>(nk));
   for (int p = 0; p < nk; ++p) kmask[size_t(p)] = model.kept_phases[size_t(p)].bits;
-  DevElim e;
+  DevElim& e = I.merr_e;
   std::vector<int> elim;
   for (int p = 0; p < nk; ++p)
     if (p != slack_pos) elim.push_back(p);
   I.upload_elim(e, yk, kmask, elim);
-  DBuf<double2> yin;
+  DBuf<double2>& yin = I.merr_yin;
   yin.alloc(yk.row.size() * 9);
   if (!yk.row.empty())
     CK(cudaMemcpyAsync(yin.p, yk.val.data(), yk.val.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
@@ -1843,7 +1917,9 @@ std::vector<double> Engine::model_errors(const ReducedModel& model) {
       rhs[size_t(l) * 6 * nk + size_t(t) * 2 + 1] = ik[size_t(t)].imag();
     }
   }
-  DBuf<double2> d_rhs, d_out, d_kv;
+  DBuf<double2>& d_rhs = I.merr_rhs;
+  DBuf<double2>& d_out = I.merr_out;
+  DBuf<double2>& d_kv = I.merr_kv;
   d_rhs.alloc(size_t(L) * 3 * nk);
   d_out.alloc(size_t(L) * 3 * nk);
   CK(cudaMemcpyAsync(d_rhs.p, rhs.data(), rhs.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
