@@ -135,6 +135,12 @@ int krg_create(const krg_network* net, const krg_scenarios* scen, int32_t device
  * the I = -conj(S/V) fixed point with device solves (scenario.cpp:52-98). */
 int krg_create_from_host(const krg_host_problem* p, int32_t device, krg_ctx** out);
 void krg_destroy(krg_ctx* ctx);
+/* Re-load a problem with the same network structure (node phases, branch
+ * endpoints) into an existing context: admittances and scenarios are copied
+ * host -> device and refactorized (AnchoredSolver ctor, solver.cpp:168-179;
+ * load_library, scenario.cpp:141-220) without re-planning the elimination or
+ * re-allocating. KRG_E_VALIDATION when the structure differs. */
+int krg_reload_from_host(krg_ctx* ctx, const krg_host_problem* p);
 /* Test hook: branch-free scorer sqrt vs IEEE __dsqrt_rn on n device-generated
  * inputs uniform in [lo, hi); returns the number of bit mismatches. */
 int krg_selftest_sqrt(int64_t n, double lo, double hi, int64_t* mismatches);

@@ -91,6 +91,7 @@ _SIGS = [
     ("krg_merge_best", C.c_int32, [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
     ("krg_create", C.c_int, [C.POINTER(KrgNetwork), C.POINTER(KrgScenarios), C.c_int32, C.POINTER(C.c_void_p)]),
     ("krg_create_from_host", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("krg_reload_from_host", C.c_int, [C.c_void_p, C.c_void_p]),
     ("krg_destroy", None, [C.c_void_p]),
     ("krg_selftest_cdiv", C.c_int, [C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double), C.c_int32]),
     ("krg_set_exchange", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, EXCHANGE_FN, C.c_void_p]),
@@ -463,6 +464,12 @@ class Context:
             self.n = problem.size
         self._h = h
         self._cb = None
+
+    def reload(self, problem: "HostProblem") -> None:
+        """krg_reload_from_host: new admittances and scenarios for the same
+        network structure, copied host -> device into this context."""
+        _check(lib().krg_reload_from_host(self._h, problem._h))
+        self.ids = problem.library.ids
 
     @property
     def L(self) -> int:

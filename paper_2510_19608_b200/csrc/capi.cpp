@@ -259,11 +259,18 @@ void check_residual(const Problem& p, const std::vector<double>& inj, const std:
 
 // Engine over a host problem: current mode solves V-hat, PQ mode runs the
 // constant-current fixed point on the device (load_library, scenario.cpp:141-220).
+void load_scenarios_from_host(Engine* eng, const Problem& p, const krg_host_problem& hp);
+
 std::unique_ptr<Engine> engine_from_host(const krg_host_problem& hp, int device) {
   Problem p = base_problem(hp.net);
   auto eng = std::make_unique<Engine>(p, device);
+  load_scenarios_from_host(eng.get(), p, hp);
+  return eng;
+}
+
+void load_scenarios_from_host(Engine* eng, const Problem& p, const krg_host_problem& hp) {
   const int L = int(hp.ids.size());
-  if (L == 0) return eng;
+  if (L == 0) return;
   std::vector<double> inj, volt;
   if (hp.pq) {
     for (size_t g = 0; g < hp.ids.size(); ++g)
@@ -283,7 +290,6 @@ std::unique_ptr<Engine> engine_from_host(const krg_host_problem& hp, int device)
   }
   check_residual(p, inj, volt, hp.ids);
   eng->set_scenarios(hp.ids, inj, volt);
-  return eng;
 }
 
 Problem problem_from(const Network& net, const ScenarioLibrary* lib) {
@@ -549,6 +555,15 @@ int krg_create_from_host(const krg_host_problem* hp, int32_t device, krg_ctx** o
   auto ctx = std::make_unique<krg_ctx>();
   ctx->eng = engine_from_host(*hp, device);
   *out = ctx.release();
+  return KRG_OK;
+  KRG_CATCH
+}
+
+int krg_reload_from_host(krg_ctx* ctx, const krg_host_problem* hp) {
+  KRG_TRY
+  Problem p = base_problem(hp->net);
+  ctx->eng->reload(p);
+  load_scenarios_from_host(ctx->eng.get(), p, *hp);
   return KRG_OK;
   KRG_CATCH
 }

@@ -1577,6 +1577,33 @@ void Engine::debug_base_refresh(int reps, double* ms, long long* clocks) {
   CK(cudaMemcpy(clocks, dbg.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost));
 }
 
+void Engine::reload(const Problem& p) {
+  // same network structure (node masks, branch endpoints, block pattern):
+  // new admittance values go straight into the resident buffers; the
+  // elimination schedule, loop graph and all allocations are kept
+  Impl& I = *impl_;
+  if (p.y.n != I.prob.y.n || p.mask != I.prob.mask || p.slack != I.prob.slack || p.y.row != I.prob.y.row ||
+      p.y.col != I.prob.y.col || p.net.branches.size() != I.prob.net.branches.size())
+    throw ValidationError("reload: the network structure differs from the context's");
+  for (size_t b = 0; b < p.net.branches.size(); ++b)
+    if (p.net.branches[b].from != I.prob.net.branches[b].from || p.net.branches[b].to != I.prob.net.branches[b].to)
+      throw ValidationError("reload: the branch list differs from the context's");
+  const std::vector<std::string> ids = I.prob.scenario_ids;
+  I.prob = p;
+  I.prob.scenario_ids = ids;
+  I.prob.L = I.L;
+  if (!p.y.val.empty())
+    CK(cudaMemcpyAsync(I.d_yin.p, p.y.val.data(), p.y.val.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
+  double sv[6];
+  for (int q = 0; q < 3; ++q) {
+    sv[2 * q] = p.net.nodes[size_t(p.slack)].slack_voltage[q].real();
+    sv[2 * q + 1] = p.net.nodes[size_t(p.slack)].slack_voltage[q].imag();
+  }
+  CK(cudaMemcpyAsync(I.d_slackv.p, sv, sizeof sv, cudaMemcpyHostToDevice, I.stream));
+  I.pivot_floor = 1e-12 * std::max(p.y.max_abs(), 1.0);
+  I.factorize(I.full, I.d_yin.p, I.pivot_floor);
+}
+
 void Engine::set_scenarios(const std::vector<std::string>& ids, const std::vector<double>& inj,
                            const std::vector<double>& volt) {
   impl_->load_scenarios(ids, inj, volt);

@@ -150,6 +150,8 @@ class Engine {
   // (then V-hat = device anchored solve of the injections)
   void set_scenarios(const std::vector<std::string>& ids, const std::vector<double>& inj,
                      const std::vector<double>& volt);
+  // new values for the same network structure (host -> device, refactorize)
+  void reload(const Problem& p);
   // constant-PQ conversion (scenario_from_pq, scenario.cpp:52-98), device solves
   void pq_to_currents(const std::vector<std::vector<std::pair<int, cx>>>& loads,
                       std::vector<double>& inj, std::vector<double>& volt);

@@ -202,3 +202,19 @@ def test_cpp_dropin_cli_matches_reference_output(tag, args, tmp_path):
         argv[6] = "-"
     subprocess.run(argv, check=True, capture_output=True)
     assert out.read_text() == path("c1", f"reduced_{tag}.json").read_text()
+
+
+def test_reload_reuses_context():
+    """krg_reload_from_host: same structure -> identical results; new scenario
+    values -> the result a fresh context computes; other structure -> error."""
+    hp = host("c1")
+    ctx = kr.Context(hp)
+    cfg = kr.ReductionConfig(e_bar=1e-3)
+    a = ctx.run_reduction(cfg)
+    ctx.reload(hp)
+    b = ctx.run_reduction(cfg)
+    assert [(t.s, t.r, bits(t.smice)) for t in a.trace] == [(t.s, t.r, bits(t.smice)) for t in b.trace]
+    rows, _ = read_trace("c1", "mag_1e-3")
+    assert [(t.s, t.r) for t in b.trace] == [(s, r) for s, r, *_ in rows]
+    with pytest.raises(kr.ValidationError):
+        ctx.reload(host("m40"))
