@@ -168,6 +168,8 @@ struct Engine::Impl {
   unsigned* h_snt = nullptr;
   // magnitude path: active-row table + candidates grouped by |phi(r)|
   DBuf<unsigned> d_tab;
+  DBuf<std::uint8_t> d_tplain;  // per 16-row tile: plain flag (score3)
+  std::vector<std::uint8_t> h_tplain;
   DBuf<int> d_cidx;
   unsigned* h_tab = nullptr;
   int* h_cidx = nullptr;
@@ -211,6 +213,7 @@ struct Engine::Impl {
     q.e_bar = cfg.e_bar;
     q.out_cand = d_pcand.p;
     q.grp_done = d_grpdone.p;
+    q.tplain = d_tplain.p;
     return q;
   }
   bool use_seg = std::getenv("KRONRED_SCORER") != nullptr && std::string(std::getenv("KRONRED_SCORER")) == "seg";
@@ -850,6 +853,7 @@ struct Engine::Impl {
     CK(cudaMallocHost(&h_cand, sizeof(int4) * size_t(2 * n)));
     CK(cudaMallocHost(&h_snt, sizeof(unsigned) * size_t(n)));
     d_tab.alloc(size_t(4) * n + size_t(nphi) + kTabPad);
+    d_tplain.alloc((size_t(4) * n + size_t(nphi) + kTabPad) / 16 + 2);
     d_cidx.alloc(size_t(2 * n));
     CK(cudaMallocHost(&h_tab, sizeof(unsigned) * (size_t(4) * n + size_t(nphi) + kTabPad)));
     CK(cudaMallocHost(&h_cidx, sizeof(int) * size_t(2 * n)));
@@ -991,6 +995,20 @@ struct Engine::Impl {
         CK(cudaMemcpyAsync(d_cidx.p, h_cidx, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
       }
       CK(cudaMemcpyAsync(d_tab.p, h_tab, size_t(R + kTabPad) * sizeof(unsigned), cudaMemcpyHostToDevice, stream));
+      {
+        const int ntiles = (R + 15) / 16;
+        h_tplain.assign(size_t(ntiles) + 1, 0);
+        for (int t = 0; t < ntiles; ++t) {
+          unsigned all = 0xffffffffu, pad = 0u;
+          for (int u = 0; u < 16; ++u) {
+            const unsigned e = h_tab[16 * t + u];
+            all &= e;
+            pad |= e & (e >> 1) & 1u;
+          }
+          h_tplain[size_t(t)] = (all & 4u) && !pad ? 1 : 0;
+        }
+        CK(cudaMemcpyAsync(d_tplain.p, h_tplain.data(), h_tplain.size(), cudaMemcpyHostToDevice, stream));
+      }
       return;
     }
     int k = 0;
@@ -1261,6 +1279,7 @@ struct Engine::Impl {
     a.sn = d_sn.p;
     a.tab_of_node = d_tabnode.p;
     a.tab = d_tab.p;
+    a.tplain = d_tplain.p;
     a.cs = d_cs.p;
     a.cr = d_cr.p;
     a.cand = d_cand.p;

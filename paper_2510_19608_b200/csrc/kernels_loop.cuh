@@ -45,6 +45,7 @@ struct LoopArgs {
   int* sn;             // [n] active super-nodes, ascending (st->ns of them)
   int* tab_of_node;    // [n] first table row of each active super-node
   unsigned* tab;       // [4n + pad] row table
+  std::uint8_t* tplain;  // [tiles of 16 rows] 1: every row a single-row super-node, no padding
   int* cs;             // [2n] candidates, lexicographic
   int* cr;
   int4* cand;          // [2n] grouped by |phi(r)|: (s, r, tab(s), tab(r))
@@ -245,6 +246,20 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     const int p = pos[g]++;
     a.cand[p] = make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
     a.cidx[p] = i;
+  }
+  // per 16-row scorer tile: plain (all first-of-super-node, no padding rows)
+  {
+    const int Rr = st->R;  // written by the last thread before the candidate section's barriers
+    const int ntiles = (Rr + 15) / 16;
+    for (int t = tid; t < ntiles; t += kLoopThreads) {
+      unsigned all = 0xffffffffu, pad = 0u;
+      for (int u = 0; u < 16; ++u) {
+        const unsigned e = a.tab[16 * t + u];
+        all &= e;
+        pad |= e & (e >> 1) & 1u;  // phase 3
+      }
+      a.tplain[t] = (all & 4u) && !pad ? 1 : 0;
+    }
   }
   if (tid == 0) {
     const int cnt3 = C - cnt1 - cnt2;

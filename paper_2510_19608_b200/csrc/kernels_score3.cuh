@@ -49,6 +49,7 @@ struct S3Args {
   double e_bar;
   double* out_cand;          // [C] per-candidate SMICE (scenario order) or -1 (infeasible)
   int* grp_done;             // [candidate groups] slice-completion counters (zeroed, self-resetting)
+  const std::uint8_t* tplain;  // [tiles] 1: the tile's 16 rows are single-row super-nodes, no padding
   int grp_start[4];          // candidate offset of each |phi(r)| group (1..3)
   int grp_cta[4];            // first CTA of each group; grp_cta[3] = CTAs in use
   const LoopState* st;       // device-resident loop: C, R and the layout come from here
@@ -139,10 +140,10 @@ __device__ __forceinline__ double s3_candidate(const double* sm, const double* m
   return feasible ? sum : -1.0;  // a feasible SMICE is never negative
 }
 
-template <int NL>
+template <int NL, int LSC>  // LSC: compile-time slice width (0: runtime a.Ls)
 __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin, int g_count, int R, double* smd,
                                         int g_base_group) {
-  const int L = a.L, Ls = a.Ls;
+  const int L = a.L, Ls = LSC ? LSC : a.Ls;
   const int Gk = a.G / NL;
   const int P = blockDim.x;
   const int tid = threadIdx.x;
@@ -278,8 +279,11 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   cp_async_wait1();
   __syncthreads();
   form_d(0);
+  bool tflag_next = a.tplain[0] != 0;
   for (int j = 0; j < ntiles; ++j) {
     const int b = j % 3;
+    const bool tflag = tflag_next;
+    if (j + 1 < ntiles) tflag_next = a.tplain[j + 1] != 0;
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
     if (fst) {
@@ -295,13 +299,21 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     const unsigned* tb = tab_s(b);
     const double2* bvp = bv_s(b) + size_t(ll) * 2;  // this thread's scenario, row stride 2*Ls
     const double2* zp = z_s(b) + size_t(gl) * NL * 2 * K3;
+    // whole plain tile (flag from the row-table builder) with no s or r row of
+    // this warp's candidates: two straight-line 8-row passes
+    if (tflag && !__any_sync(0xffffffffu, j == (ts0 >> 4) || j == (tr0 >> 4))) {
+      constexpr int NRT = NL == 1 ? 8 : 4;  // rows per pass (register budget)
+#pragma unroll 1
+      for (int h = 0; h < K3 / NRT; ++h) s3_plain<NL, NRT>(bvp, zp, RS, NRT * h, cv, smice, cm, mx);
+      continue;
+    }
     int q = 0;
 #pragma unroll 1
     while (q < K3 / 4) {
       const int blk = (t0 >> 2) + q;
       const uint4 e4 = *reinterpret_cast<const uint4*>(tb + 4 * q);
       const bool fast = s3_block_plain(e4) && !__any_sync(0xffffffffu, blk == sblk || blk == rblk);
-      if (fast && q + 1 < K3 / 4) {
+      if (NL == 1 && fast && q + 1 < K3 / 4) {
         const uint4 f4 = *reinterpret_cast<const uint4*>(tb + 4 * q + 4);
         if (s3_block_plain(f4) && !__any_sync(0xffffffffu, blk + 1 == sblk || blk + 1 == rblk)) {
           s3_plain<NL, 8>(bvp, zp, RS, 4 * q, cv, smice, cm, mx);
@@ -419,11 +431,11 @@ __global__ void __launch_bounds__(256) score3_kernel(S3Args a) {
     // counter slot: global candidate-group index (every group range is a
     // whole number of nsl-slice items)
     if (w < gc[1])
-      s3_body<1>(a, w, gs[1], gs[2] - gs[1], R, sm_dyn, 0);
+      s3_body<1, 0>(a, w, gs[1], gs[2] - gs[1], R, sm_dyn, 0);
     else if (w < gc[2])
-      s3_body<2>(a, w - gc[1], gs[2], gs[3] - gs[2], R, sm_dyn, gc[1] / a.nsl);
+      s3_body<2, 0>(a, w - gc[1], gs[2], gs[3] - gs[2], R, sm_dyn, gc[1] / a.nsl);
     else
-      s3_body<3>(a, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
+      s3_body<3, 0>(a, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
     __syncthreads();  // shared memory is reused by the next item
   }
 }
