@@ -140,6 +140,80 @@ __device__ __forceinline__ double s3_candidate(const double* sm, const double* m
   return feasible ? sum : -1.0;  // a feasible SMICE is never negative
 }
 
+
+// Row context of the general (non-plain) passes: the candidate's s rows merge
+// r's member bounds, r's rows and padding rows contribute nothing.
+struct S3Fix {
+  int ts0, ts1, tr0, tr1;
+  double rlo0, rlo1, rlo2, rhi0, rhi1, rhi2;
+};
+
+// NR rows of a non-plain tile, still on the fast sqrt path. Per row (t =
+// table row, e = table entry):
+//   em = max(m - lo, hi - m)                              cluster error
+//   s row: em = max(em, m - rlo_p, rhi_p - m)             = max(m - min(lo, rlo_p), max(hi, rhi_p) - m)
+//          exactly, rounded subtraction being monotone (reduce.cpp:114-115)
+//   r row or padding row: em = 0                          (reduce.cpp:111; +0 is an exact no-op below)
+//   fold driven by the first-of-super-node bit            (reduce.cpp:110-121)
+// A zero current c_p adds (+-0) to Vc, which leaves |Vc| bit-identical for
+// finite Z, so the reference's skip (reduce.cpp:227) needs no branch here.
+template <int NL, int NR>
+__device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, const double2* __restrict__ zp, int RS,
+                                            int u0, int t0, const unsigned* tb, const C2 (&cv)[NL], const S3Fix& f,
+                                            double& smice, double& cm, double& mx) {
+  double em[NR];
+  bool bad = false;
+  auto fix = [&](int v, double m, double e) {
+    const int t = t0 + u0 + v;
+    const unsigned ph = tb[u0 + v] & 3u;
+    if (t >= f.ts0 && t < f.ts1 && ph != 3u) {
+      const double rl = ph == 0u ? f.rlo0 : (ph == 1u ? f.rlo1 : f.rlo2);
+      const double rh = ph == 0u ? f.rhi0 : (ph == 1u ? f.rhi1 : f.rhi2);
+      e = dmax(e, dmax(dev::dsub(m, rl), dev::dsub(rh, m)));
+    }
+    return ((t >= f.tr0 && t < f.tr1) || ph == 3u) ? 0.0 : e;
+  };
+#pragma unroll
+  for (int v = 0; v < NR; ++v) {
+    const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+    double vx = b0.x, vy = b0.y;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const double2 dz = zp[(k * 2) * K3 + u0 + v];
+      vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
+      vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
+    }
+    const double s2 = dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy));
+    bad = bad || !sqrt_fast_ok(s2);
+    const double m = sqrt_rn_fast(s2);
+    em[v] = fix(v, m, dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m)));
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+#pragma unroll
+    for (int v = 0; v < NR; ++v) {
+      const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+      double vx = b0.x, vy = b0.y;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        const double2 dz = zp[(k * 2) * K3 + u0 + v];
+        vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
+        vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
+      }
+      const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
+      em[v] = fix(v, m, dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m)));
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NR; ++v) {
+    if (tb[u0 + v] & 4u) {
+      smice = dev::dadd(smice, cm);
+      cm = 0.0;
+    }
+    cm = dmax(cm, em[v]);
+    mx = dmax(mx, em[v]);
+  }
+}
+
 template <int NL, int LSC>  // LSC: compile-time slice width (0: runtime a.Ls)
 __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin, int g_count, int R, double* smd,
                                         int g_base_group) {
@@ -165,7 +239,6 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   const int4 cd = a.cand[c];
   const int s = cd.x, r = cd.y;
   const int ts0 = cd.z, tr0 = cd.w;
-  const int sblk = ts0 >> 2, rblk = tr0 >> 2;  // a super-node's rows share one 4-row block
   const unsigned ms = a.mask[s], mr = a.mask[r];
   const int ts1 = ts0 + __popc(ms), tr1 = tr0 + NL;
   const int rs0 = a.prow_off[s], rr0 = a.prow_off[r];
@@ -194,6 +267,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     }
   }
   __syncthreads();
+  const S3Fix fx{ts0, ts1, tr0, tr1, rlo0, rlo1, rlo2, rhi0, rhi1, rhi2};
   const size_t nphi = size_t(a.nphi);
   const int ntiles = (R + K3 - 1) / K3;
   // (base, bounds) slice staging: each row is 2*Ls contiguous 16-byte chunks
@@ -300,64 +374,17 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     const double2* bvp = bv_s(b) + size_t(ll) * 2;  // this thread's scenario, row stride 2*Ls
     const double2* zp = z_s(b) + size_t(gl) * NL * 2 * K3;
     // whole plain tile (flag from the row-table builder) with no s or r row of
-    // this warp's candidates: two straight-line 8-row passes
+    // this warp's candidates: straight-line passes with the all-first fold;
+    // any other tile: the same fast passes with per-row fixups and a
+    // flag-driven fold
+    constexpr int NRT = NL == 1 ? 8 : 4;  // rows per pass (register budget)
     if (tflag && !__any_sync(0xffffffffu, j == (ts0 >> 4) || j == (tr0 >> 4))) {
-      constexpr int NRT = NL == 1 ? 8 : 4;  // rows per pass (register budget)
 #pragma unroll 1
-      for (int h = 0; h < K3 / NRT; ++h) s3_plain<NL, NRT>(bvp, zp, RS, NRT * h, cv, smice, cm, mx);
-      continue;
-    }
-    int q = 0;
+      for (int hh = 0; hh < K3 / NRT; ++hh) s3_plain<NL, NRT>(bvp, zp, RS, NRT * hh, cv, smice, cm, mx);
+    } else {
 #pragma unroll 1
-    while (q < K3 / 4) {
-      const int blk = (t0 >> 2) + q;
-      const uint4 e4 = *reinterpret_cast<const uint4*>(tb + 4 * q);
-      const bool fast = s3_block_plain(e4) && !__any_sync(0xffffffffu, blk == sblk || blk == rblk);
-      if (NL == 1 && fast && q + 1 < K3 / 4) {
-        const uint4 f4 = *reinterpret_cast<const uint4*>(tb + 4 * q + 4);
-        if (s3_block_plain(f4) && !__any_sync(0xffffffffu, blk + 1 == sblk || blk + 1 == rblk)) {
-          s3_plain<NL, 8>(bvp, zp, RS, 4 * q, cv, smice, cm, mx);
-          q += 2;
-          continue;
-        }
-      }
-      if (fast) {
-        s3_plain<NL, 4>(bvp, zp, RS, 4 * q, cv, smice, cm, mx);
-      } else {
-        // general block: padding, multi-row super-nodes, the candidate's s
-        // (bounds merged with r's, reduce.cpp:114-115) and r (skipped, :111)
-        const int u0 = 4 * q;
-        const unsigned e[4] = {e4.x, e4.y, e4.z, e4.w};
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int t = t0 + u0 + v;
-          const unsigned ev = e[v];
-          const unsigned ph = ev & 3u;
-          const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
-          double vx = b0.x, vy = b0.y;
-#pragma unroll
-          for (int k = 0; k < NL; ++k) {
-            if (dev::cis0(cv[k])) continue;  // reduce.cpp:227: a zero current adds nothing
-            const double2 dz = zp[(k * 2) * K3 + u0 + v];
-            vx = dev::dadd(vx, dev::dsub(dev::dmul(cv[k].x, dz.x), dev::dmul(cv[k].y, dz.y)));
-            vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
-          }
-          const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
-          double lo = b1.x, hi = b1.y;
-          if (t >= ts0 && t < ts1 && ph != 3u) {
-            lo = dmin(lo, ph == 0u ? rlo0 : (ph == 1u ? rlo1 : rlo2));
-            hi = dmax(hi, ph == 0u ? rhi0 : (ph == 1u ? rhi1 : rhi2));
-          }
-          const double e_v = ((t >= tr0 && t < tr1) || ph == 3u) ? 0.0 : dmax(dev::dsub(m, lo), dev::dsub(hi, m));
-          if (ev & 4u) {
-            smice = dev::dadd(smice, cm);
-            cm = 0.0;
-          }
-          cm = dmax(cm, e_v);
-          mx = dmax(mx, e_v);
-        }
-      }
-      ++q;
+      for (int hh = 0; hh < K3 / NRT; ++hh)
+        s3_rows_gen<NL, NRT>(bvp, zp, RS, NRT * hh, t0, tb, cv, fx, smice, cm, mx);
     }
   }
   smice = dev::dadd(smice, cm);
@@ -407,7 +434,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   }
 }
 
-__global__ void __launch_bounds__(256) score3_kernel(S3Args a) {
+__global__ void __launch_bounds__(128, 3) score3_kernel(S3Args a) {
   extern __shared__ double sm_dyn[];
   const int b = blockIdx.x;
   int C = a.C, R = a.R;
