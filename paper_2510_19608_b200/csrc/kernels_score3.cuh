@@ -60,7 +60,9 @@ struct S3Layout {
   int Ls, G;
   __host__ __device__ size_t tab_e() const { return (K3 * 4 + 15) / 16; }  // double2 units
   __host__ __device__ size_t bv_e() const { return size_t(Ls) * K3 * 2; }
-  __host__ __device__ size_t z_e() const { return size_t(G) * 2 * K3; }    // Zs and Zr staging
+  // Zs and Zr staging; each candidate's block padded by one 16-byte slot so
+  // the candidates of a warp hit different banks
+  __host__ __device__ size_t z_e() const { return size_t(G) * (2 * K3 + 1); }
   __host__ __device__ size_t buf_e() const { return tab_e() + bv_e() + z_e(); }
   __host__ __device__ size_t smem_bytes() const { return 3 * buf_e() * sizeof(double2) + size_t(G) * 2 * sizeof(int) + 64; }
 };
@@ -74,7 +76,7 @@ __device__ __forceinline__ void s3_plain(const double2* __restrict__ bvp, const 
   bool bad = false;
 #pragma unroll
   for (int v = 0; v < NR; ++v) {
-    const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+    const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + (RS >> 1)];
     double vx = b0.x, vy = b0.y;
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
@@ -90,7 +92,7 @@ __device__ __forceinline__ void s3_plain(const double2* __restrict__ bvp, const 
   if (__any_sync(0xffffffffu, bad)) {
 #pragma unroll
     for (int v = 0; v < NR; ++v) {
-      const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+      const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + (RS >> 1)];
       double vx = b0.x, vy = b0.y;
 #pragma unroll
       for (int k = 0; k < NL; ++k) {
@@ -175,7 +177,7 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
   };
 #pragma unroll
   for (int v = 0; v < NR; ++v) {
-    const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+    const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + (RS >> 1)];
     double vx = b0.x, vy = b0.y;
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
@@ -191,7 +193,7 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
   if (__any_sync(0xffffffffu, bad)) {
 #pragma unroll
     for (int v = 0; v < NR; ++v) {
-      const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + 1];
+      const double2 b0 = bvp[(u0 + v) * RS], b1 = bvp[(u0 + v) * RS + (RS >> 1)];
       double vx = b0.x, vy = b0.y;
 #pragma unroll
       for (int k = 0; k < NL; ++k) {
@@ -275,6 +277,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   const int nsc = min(Ls, L - sl * Ls);  // scenarios of this slice
   const bool bv_fixed = (P % RS) == 0;
   const int bv_ch = tid % RS, bv_u0 = tid / RS, bv_du = P / RS;
+  const int bv_dst = (bv_ch & 1) * Ls + (bv_ch >> 1);  // shared row layout [base x Ls][bounds x Ls]
   const size_t bv_off = size_t(sl) * Ls * 2;
 
   auto stage = [&](int j, int b) {
@@ -284,14 +287,14 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
       if (bv_ch < 2 * nsc)
         for (int u = bv_u0; u < K3; u += bv_du) {
           const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-          cp_async16(bv_s(b) + size_t(u) * RS + bv_ch, a.bv + rho * 2 * L + bv_off + bv_ch);
+          cp_async16(bv_s(b) + size_t(u) * RS + bv_dst, a.bv + rho * 2 * L + bv_off + bv_ch);
         }
     } else {
       for (int i = tid; i < K3 * RS; i += P) {
         const int u = i / RS, ch = i - u * RS;
         if (ch >= 2 * nsc) continue;
         const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-        cp_async16(bv_s(b) + size_t(u) * RS + ch, a.bv + rho * 2 * L + bv_off + ch);
+        cp_async16(bv_s(b) + size_t(u) * RS + (ch & 1) * Ls + (ch >> 1), a.bv + rho * 2 * L + bv_off + ch);
       }
     }
     const int nz = Gk * NL * 2 * K3;
@@ -299,7 +302,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
       const int u = i % K3;
       const int col = zcol[i / K3];
       const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-      cp_async16(z_s(b) + i, a.Z + size_t(col) * nphi + rho);
+      cp_async16(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(col) * nphi + rho);
     }
   };
   // Fast staging: each thread owns at most two bv rows and one Z row of every
@@ -317,19 +320,22 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     const int t0 = j * K3;
     if (tid < K3 / 4) cp_async16(tab_s(b) + 4 * tid, a.tab + t0 + 4 * tid);
     if (bv_ch < 2 * nsc) {
-      if (u_a < K3) cp_async16(bv_s(b) + size_t(u_a) * RS + bv_ch, a.bv + size_t(rr[0]) * 2 * L + bv_off + bv_ch);
-      if (u_b < K3) cp_async16(bv_s(b) + size_t(u_b) * RS + bv_ch, a.bv + size_t(rr[1]) * 2 * L + bv_off + bv_ch);
+      if (u_a < K3) cp_async16(bv_s(b) + size_t(u_a) * RS + bv_dst, a.bv + size_t(rr[0]) * 2 * L + bv_off + bv_ch);
+      if (u_b < K3) cp_async16(bv_s(b) + size_t(u_b) * RS + bv_dst, a.bv + size_t(rr[1]) * 2 * L + bv_off + bv_ch);
     }
     const int nz = Gk * NL * 2 * K3;
-    for (int i = tid; i < nz; i += P) cp_async16(z_s(b) + i, a.Z + size_t(zcol[i / K3]) * nphi + rr[2]);
+    for (int i = tid; i < nz; i += P)
+      cp_async16(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(zcol[i / K3]) * nphi + rr[2]);
   };
   auto form_d = [&](int b) {  // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row)
     double2* zz = z_s(b);
     const int nd = Gk * NL * K3;
     for (int i = tid; i < nd; i += P) {
       const int col2 = i / K3, u = i - col2 * K3;
-      const double2 za = zz[(col2 * 2 + 0) * K3 + u], zr = zz[(col2 * 2 + 1) * K3 + u];
-      zz[(col2 * 2 + 0) * K3 + u] = make_double2(dev::dsub(za.x, zr.x), dev::dsub(za.y, zr.y));
+      const int g = col2 / NL;  // candidate: its block starts at g * (NL * 2 * K3 + 1)
+      double2* zc = zz + g * (NL * 2 * K3 + 1) + (col2 - g * NL) * 2 * K3;
+      const double2 za = zc[u], zr = zc[K3 + u];
+      zc[u] = make_double2(dev::dsub(za.x, zr.x), dev::dsub(za.y, zr.y));
     }
   };
 
@@ -371,8 +377,8 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     if (j + 1 < ntiles) form_d((j + 1) % 3);
     const int t0 = j * K3;
     const unsigned* tb = tab_s(b);
-    const double2* bvp = bv_s(b) + size_t(ll) * 2;  // this thread's scenario, row stride 2*Ls
-    const double2* zp = z_s(b) + size_t(gl) * NL * 2 * K3;
+    const double2* bvp = bv_s(b) + size_t(ll);  // this thread's scenario: base at +0, bounds at +Ls per row
+    const double2* zp = z_s(b) + size_t(gl) * (NL * 2 * K3 + 1);
     // whole plain tile (flag from the row-table builder) with no s or r row of
     // this warp's candidates: straight-line passes with the all-first fold;
     // any other tile: the same fast passes with per-row fixups and a
