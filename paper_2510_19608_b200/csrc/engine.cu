@@ -142,7 +142,8 @@ enum IntArr {
   A_APPLY_SLOTS, A_COUNT
 };
 
-constexpr int kTabPad = kTabPadRows;  // row-table padding >= largest scorer tile (S*4 rows)
+constexpr int kTabPad = kTabPadRows;
+constexpr int kLoopUnroll = 4;  // loop iterations per conditional-graph body  // row-table padding >= largest scorer tile (S*4 rows)
 
 struct Engine::Impl {
   Problem prob;
@@ -159,6 +160,8 @@ struct Engine::Impl {
   double pivot_floor = 0;
   DevElim full;               // anchored factorization of Y
   DBuf<double2> d_inj, d_vhat, d_v0, d_v0p, d_vhatp, d_iagg, d_iaggp, d_bv, d_Z, d_slackv;
+  DBuf<double2> d_tfwd;  // [L][nphi] forward values of the last base refresh
+  bool force_full_refresh = std::getenv("KRONRED_FULL_REFRESH") != nullptr;
   std::vector<double> h_vhat;  // [L][3n][2]
   // per-iteration inputs (pinned staging)
   DBuf<int4> d_cand;
@@ -459,6 +462,7 @@ struct Engine::Impl {
       std::vector<int> bm, fe2, be2;
       const int zero_cf = int(g.size());
       g.push_back(-1);  // one exact-zero coefficient for pull-free steps
+      std::vector<int> frec_of_step(size_t(std::max(h.nsteps, 1)), -1);
       auto slots = [&](const std::vector<int>& off, const std::vector<int>& steps, bool fwd, int& nrounds,
                        std::vector<int>& recs, std::vector<int>& ext, std::vector<int>& ents) {
         nrounds = 0;
@@ -478,6 +482,7 @@ struct Engine::Impl {
               const int st = steps[size_t(c0 + r0 + ln)];
               const int k = h.step_node[size_t(st)];
               const int mk = __builtin_popcount(h.mask[size_t(k)]);
+              if (fwd) frec_of_step[size_t(st)] = int(recs.size() / 4);
               const int first = fwd ? fin_first[size_t(st)] : bcp_first[size_t(st)];
               const int ne = fwd ? h.in_off[size_t(st) + 1] - h.in_off[size_t(st)]
                                  : h.cpl_off[size_t(st) + 1] - h.cpl_off[size_t(st)];
@@ -547,6 +552,23 @@ struct Engine::Impl {
         kp.push_back(int(kk));
       }
       B.kept = put4(kp);
+      // incremental forward walk: per node {forward record, elimination-tree
+      // parent, step index}; only for trees (every node feeds one later node)
+      {
+        std::vector<int> wk(size_t(nn) * 4, -1);
+        bool tree = h.nsteps > 0;
+        for (int st = 0; st < h.nsteps; ++st) {
+          const int k = h.step_node[size_t(st)];
+          wk[size_t(k) * 4 + 0] = frec_of_step[size_t(st)];
+          wk[size_t(k) * 4 + 2] = st;
+          for (int e = h.in_off[size_t(st)]; e < h.in_off[size_t(st) + 1]; ++e) {
+            const int j = h.in_node[size_t(e)];
+            if (wk[size_t(j) * 4 + 1] >= 0) tree = false;
+            wk[size_t(j) * 4 + 1] = k;
+          }
+        }
+        B.walk = tree ? put4(wk) : -1;
+      }
       while (bm.size() % 4) bm.push_back(0);
       B.nfr = nfr;
       B.nbr = nbr;
@@ -558,12 +580,14 @@ struct Engine::Impl {
       CK(cudaMemcpyAsync(d.bmeta.p, bm.data(), bm.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
       const size_t fixed = size_t(B.ncf) * 16 + size_t(B.nmeta) * 4;
       d.bW = 0;
+      // two nph-row buffers per warp when the incremental walk is available
+      const size_t per_warp = size_t(nph) * 16 * (B.walk >= 0 ? 2 : 1);
       for (int w = 8; w >= 1; --w)
-        if (fixed + size_t(w) * size_t(nph) * 16 <= size_t(optin_smem) - 64) {
+        if (fixed + size_t(w) * per_warp <= size_t(optin_smem) - 64) {
           d.bW = w;
           break;
         }
-      d.bsmem = int(fixed + size_t(std::max(d.bW, 1)) * size_t(nph) * 16);
+      d.bsmem = int(fixed + size_t(std::max(d.bW, 1)) * per_warp);
     }
     d.meta.alloc(meta.size());
     if (!meta.empty())
@@ -730,7 +754,8 @@ struct Engine::Impl {
 
   // refresh_base (reduce.cpp:265-268): base = solve(i_agg) for every scenario
   long long* dbg_clock = nullptr;
-  void refresh_base() {
+  // s, r >= 0: the commit that changed i_agg (incremental forward walk)
+  void refresh_base(int s = -1, int r = -1) {
     if (full.bW > 0) {
       BaseArgs b = full.bprog;
       b.L = L;
@@ -741,6 +766,10 @@ struct Engine::Impl {
       b.kept_val = d_slackv.p;
       b.bv = d_bv.p;
       b.dbg = dbg_clock;
+      b.tfwd = b.walk >= 0 ? d_tfwd.p : nullptr;
+      b.inc = (b.walk >= 0 && s >= 0 && !force_full_refresh) ? 1 : 0;
+      b.inc_s = s;
+      b.inc_r = r;
       if (profile) CK(cudaEventRecord(ev_a, stream));
       base_refresh_kernel<<<(L + b.W - 1) / b.W, 32 * b.W, full.bsmem, stream>>>(b);
       launched();
@@ -889,6 +918,7 @@ struct Engine::Impl {
     d_bv.alloc(size_t(nphi) * L * 2);
     d_iagg.alloc(size_t(n) * L * 3);
     d_iaggp.alloc(size_t(L) * std::max(nphi, 1));
+    d_tfwd.alloc(size_t(L) * std::max(nphi, 1));
     d_psmice.alloc(size_t(s3_ldc()) * L);
     d_pmaxerr.alloc(size_t(s3_ldc()) * L);
     d_grpdone.alloc(size_t(s3_ldc()) / 4 + 8);
@@ -1387,6 +1417,8 @@ struct Engine::Impl {
     bb.dbg = nullptr;
     bb.st = d_loopst.p;
     bb.tdbg = la.tdbg;
+    bb.tfwd = bb.walk >= 0 ? d_tfwd.p : nullptr;
+    bb.inc = (bb.walk >= 0 && !force_full_refresh) ? 1 : 0;
     // first enumeration (also stamps the loop start)
     enum_kernel<<<1, kLoopThreads, enum_smem(), stream>>>(la);
     launched();
@@ -1414,6 +1446,10 @@ struct Engine::Impl {
       lb.use_cond = 1;
       lb.cond = h;
       CK(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      // kLoopUnroll iterations per body execution: the conditional relaunch
+      // costs a few microseconds, and iterations after the last one are
+      // early-exit no-ops (every kernel checks st->done)
+      for (int u = 0; u < kLoopUnroll; ++u) {
       if (use_score3) {
         S3Args q = s3_args();
         q.st = d_loopst.p;
@@ -1437,6 +1473,7 @@ struct Engine::Impl {
       base_refresh_kernel<<<(L + bb.W - 1) / bb.W, 32 * bb.W, full.bsmem, stream>>>(bb);
       CK(cudaEventRecord(ev_join, stream2));
       CK(cudaStreamWaitEvent(stream, ev_join, 0));
+      }
       CK(cudaStreamEndCapture(stream, &body));
       CK(cudaGraphInstantiate(&loop_exec, graph, 0));
       loop_graph = graph;
@@ -1468,13 +1505,13 @@ struct Engine::Impl {
     CK(cudaStreamSynchronize(stream));
     check_deferred_fail();
     const LoopState st = *h_loopst;
-    launches += 4LL * (st.iter + 1);
+    launches += 4LL * ((st.iter + kLoopUnroll) / kLoopUnroll * kLoopUnroll);
     const int it = st.iter;
     if (loop_trace && it > 2) {
       std::vector<unsigned long long> T(size_t(n + 1) * 8);
       CK(cudaMemcpy(T.data(), d_tdbg.p, sizeof(unsigned long long) * T.size(), cudaMemcpyDeviceToHost));
       // per iteration i: score start [i][6], pick [i][0..1], enum for i+1 [i+1][2..3], refresh [i+1][4..5]
-      double a_sc = 0, a_pick = 0, a_p2e = 0, a_enum = 0, a_p2r = 0, a_r2s = 0, a_e2s = 0;
+      double a_sc = 0, a_pick = 0, a_p2e = 0, a_enum = 0, a_p2r = 0, a_r2s = 0, a_e2s = 0, a_ref = 0, a_tab = 0;
       int cnt = 0;
       for (int i = 1; i + 1 < it; ++i) {
         const unsigned long long* c = &T[size_t(i) * 8];
@@ -1486,13 +1523,16 @@ struct Engine::Impl {
         a_p2r += double(nx[4] - c[1]);
         a_r2s += double(nx[6] - nx[4]);
         a_e2s += double(nx[6] - nx[3]);
+        a_ref += double(nx[5] - nx[4]);
+        a_tab += double(nx[7] - nx[2]);
         ++cnt;
       }
       std::fprintf(stderr,
-                   "loop timeline (us/iter avg over %d): score+gap %.1f | pick %.1f | pick->enum %.1f enum %.1f | "
-                   "pick->refresh %.1f refresh-start->next score %.1f | enum-end->next score %.1f\n",
-                   cnt, a_sc / cnt / 1e3, a_pick / cnt / 1e3, a_p2e / cnt / 1e3, a_enum / cnt / 1e3, a_p2r / cnt / 1e3,
-                   a_r2s / cnt / 1e3, a_e2s / cnt / 1e3);
+                   "loop timeline (us/iter avg over %d): score+gap %.1f | pick %.1f | pick->enum %.1f enum %.1f (table %.1f) | "
+                   "pick->refresh %.1f refresh-start->next score %.1f (refresh block0 %.1f) | enum-end->next score %.1f\n",
+                   cnt, a_sc / cnt / 1e3, a_pick / cnt / 1e3, a_p2e / cnt / 1e3, a_enum / cnt / 1e3, a_tab / cnt / 1e3,
+                   a_p2r / cnt / 1e3,
+                   a_r2s / cnt / 1e3, a_ref / cnt / 1e3, a_e2s / cnt / 1e3);
     }
     tr_s.resize(size_t(it));
     tr_r.resize(size_t(it));
@@ -1531,7 +1571,7 @@ struct Engine::Impl {
                                                        d_iagg.p, d_bv.p, d_iaggp.p, nphi);
     launched();
     CK(cudaGetLastError());
-    refresh_base();
+    refresh_base(s, r);
   }
 };
 
@@ -1585,12 +1625,17 @@ void Engine::debug_base_refresh(int reps, double* ms, long long* clocks) {
   dbg.alloc(4);
   CK(cudaMemset(dbg.p, 0, 4 * sizeof(long long)));
   I.ensure_events();
+  // reps < 0: time the incremental refresh after the first candidate's
+  // commit pattern (the walk from its s and r; values are not meaningful)
+  const bool inc = reps < 0;
+  if (inc) reps = -reps;
+  const int s = inc && !I.cs.empty() ? I.cs[0] : -1, r = inc && !I.cr.empty() ? I.cr[0] : -1;
   I.refresh_base();
   CK(cudaEventRecord(I.ev_a, I.stream));
-  for (int i = 0; i < reps; ++i) I.refresh_base();
+  for (int i = 0; i < reps; ++i) I.refresh_base(s, r);
   *ms = I.event_ms() / reps;
   I.dbg_clock = dbg.p;
-  I.refresh_base();
+  I.refresh_base(s, r);
   CK(cudaStreamSynchronize(I.stream));
   I.dbg_clock = nullptr;
   CK(cudaMemcpy(clocks, dbg.p, 4 * sizeof(long long), cudaMemcpyDeviceToHost));

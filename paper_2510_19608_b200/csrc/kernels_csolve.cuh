@@ -26,6 +26,7 @@ enum CMode { CM_FULL = 0, CM_BASE = 1, CM_ZCOL = 2 };
 // the pick/commit kernel and the base refresh (which all exit when done).
 struct LoopState {
   int done, iter, ns, C, R, err;
+  int last_s, last_r;  // the last committed candidate (incremental base refresh)
   int grp_start[4];  // candidate offset of each |phi(r)| group (index 1..3)
   int grp_cta[4];    // first CTA of each group; grp_cta[3] = CTAs in use
 };
@@ -383,6 +384,13 @@ struct BaseArgs {
   long long* dbg;
   const LoopState* st;    // device-resident loop: skip once the loop is done
   unsigned long long* tdbg;  // optional loop timeline [iter][8] (slots 4, 5)
+  // incremental forward sweep: only the elimination-tree ancestors of the two
+  // rows a commit changed are re-eliminated; the other nodes' forward values
+  // are bit-identical to the previous refresh and come from tfwd
+  double2* tfwd;          // [L][nphi] forward values of the last refresh (null: disabled)
+  int inc;                // 1: incremental (s, r below or st->last_s/last_r), 0: full sweep
+  int inc_s, inc_r;       // changed nodes (host-driven loop)
+  int walk;               // ints offset in M of [node] int4 {record, parent, step, 0} (-1 record: kept)
 };
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -436,12 +444,19 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   if (tid == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const unsigned bytes = unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u + unsigned(nw) * unsigned(a.nphi) * 16u;
+    // incremental: x <- last forward values, and the right-hand sides of the
+    // re-eliminated path nodes come from a second buffer (both TMA-staged)
+    const unsigned per = unsigned(a.nphi) * 16u;
+    const unsigned bytes = unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u + unsigned(nw) * per * (a.inc ? 2u : 1u);
     mbar_expect_tx(&bar, bytes);
     if (a.ncf) bulk_g2s(cf, a.cfac, unsigned(a.ncf) * 16u, &bar);
     bulk_g2s(M, a.meta, unsigned(a.nmeta) * 4u, &bar);
+    const double2* src = a.inc ? a.tfwd : a.iaggp;
     for (int w = 0; w < nw; ++w)
-      bulk_g2s(xall + size_t(w) * a.nphi, a.iaggp + size_t(blockIdx.x * a.W + w) * a.nphi, unsigned(a.nphi) * 16u, &bar);
+      bulk_g2s(xall + size_t(w) * a.nphi, src + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
+    if (a.inc)
+      for (int w = 0; w < nw; ++w)
+        bulk_g2s(xall + size_t(a.W + w) * a.nphi, a.iaggp + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -464,75 +479,106 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
   const int4* fx = reinterpret_cast<const int4*>(M + a.fext);
   const int2* fe = reinterpret_cast<const int2*>(M + a.fent);
-  int4 rc = fs[lane];
-  int4 rx = fx[lane];
-  for (int fr = 0; fr < a.nfr; ++fr) {
-    const int4 nx = fs[(fr + 1) * 32 + lane];
-    const int4 nxx = fx[(fr + 1) * 32 + lane];
+  auto fwd_step = [&](const int4 rc, const int4 rx) {
     if (rc.x >= 0 && rc.z >= 0) {
-      // scalar step: two pulls inline (zero pulls when absent), their
-      // products in flight together; the subtractions keep elimination order
-      const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y);
-      const C2 t1 = lds2(xs + rx.x), a1 = lds2(cs + rx.y);
-      const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
-      const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
-      C2 b = dev::csub(dev::csub(b0, u0), u1);
-      int e = rx.z;
-      const int e_end = rx.z + rx.w;
+        // scalar step: two pulls inline (zero pulls when absent), their
+        // products in flight together; the subtractions keep elimination order
+        const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y);
+        const C2 t1 = lds2(xs + rx.x), a1 = lds2(cs + rx.y);
+        const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
+        const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
+        C2 b = dev::csub(dev::csub(b0, u0), u1);
+        int e = rx.z;
+        const int e_end = rx.z + rx.w;
 #pragma unroll 1
-      for (; e < e_end; e += 3) {  // further children, predicated batches of three
-        C2 u[3];
+        for (; e < e_end; e += 3) {  // further children, predicated batches of three
+          C2 u[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const int2 en = fe[min(e + q, e_end - 1)];
-          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
+          for (int q = 0; q < 3; ++q) {
+            const int2 en = fe[min(e + q, e_end - 1)];
+            u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
+          }
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (e + q < e_end) b = dev::csub(b, u[q]);
         }
+        sts2(xs + rc.x, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, b)));
+      } else if (rc.x >= 0) {
+        const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
+        C2 b[3];
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
-          if (e + q < e_end) b = dev::csub(b, u[q]);
-      }
-      sts2(xs + rc.x, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, b)));
-    } else if (rc.x >= 0) {
-      const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
-      C2 b[3];
+        for (int i = 0; i < 3; ++i) b[i] = i < mk ? ld2(x + xk + i) : C2{0.0, 0.0};
+        for (int e = rx.z; e < rx.z + rx.w; ++e) {
+          const int2 en = fe[e];
+          const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+          C2 tj[3];
 #pragma unroll
-      for (int i = 0; i < 3; ++i) b[i] = i < mk ? ld2(x + xk + i) : C2{0.0, 0.0};
-      for (int e = rx.z; e < rx.z + rx.w; ++e) {
-        const int2 en = fe[e];
-        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
-        C2 tj[3];
+          for (int c = 0; c < 3; ++c) tj[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
 #pragma unroll
-        for (int c = 0; c < 3; ++c) tj[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
+          for (int r = 0; r < 3; ++r) {
+            if (r >= mk) continue;
+            C2 acc = {0.0, 0.0};
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (c < mj) acc = dev::cadd(acc, dev::cmul(ld2(cf + bo + r * mj + c), tj[c]));
+            b[r] = dev::csub(b[r], acc);
+          }
+        }
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
           if (r >= mk) continue;
           C2 acc = {0.0, 0.0};
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            if (c < mj) acc = dev::cadd(acc, dev::cmul(ld2(cf + bo + r * mj + c), tj[c]));
-          b[r] = dev::csub(b[r], acc);
+            if (c < mk) acc = dev::cadd(acc, dev::cmul(ld2(cf + po + r * mk + c), b[c]));
+          st2(x + xk + r, acc);
         }
       }
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        if (r >= mk) continue;
-        C2 acc = {0.0, 0.0};
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (c < mk) acc = dev::cadd(acc, dev::cmul(ld2(cf + po + r * mk + c), b[c]));
-        st2(x + xk + r, acc);
-      }
+  };
+  if (!a.inc) {
+    int4 rc = fs[lane];
+    int4 rx = fx[lane];
+    for (int fr = 0; fr < a.nfr; ++fr) {
+      const int4 nx = fs[(fr + 1) * 32 + lane];
+      const int4 nxx = fx[(fr + 1) * 32 + lane];
+      fwd_step(rc, rx);
+      rc = nx;
+      rx = nxx;
+      __syncwarp();
     }
-    rc = nx;
-    rx = nxx;
-    __syncwarp();
+    if (a.tfwd)  // keep the forward values for the next (incremental) refresh
+      for (int r = lane; r < a.nphi; r += 32) a.tfwd[size_t(rhs) * a.nphi + r] = x[r];
+  } else if (lane == 0) {
+    // walk the ancestors of the two changed nodes in elimination order
+    const int4* W = reinterpret_cast<const int4*>(M + a.walk);
+    int na = a.st ? a.st->last_s : a.inc_s, nb = a.st ? a.st->last_r : a.inc_r;
+    if (na >= 0 && W[na].x < 0) na = -1;  // kept (slack): no forward step
+    if (nb >= 0 && W[nb].x < 0) nb = -1;
+    while (na >= 0 || nb >= 0) {
+      const int sa = na >= 0 ? W[na].z : 0x7fffffff, sb = nb >= 0 ? W[nb].z : 0x7fffffff;
+      const int k = sa <= sb ? na : nb;
+      const int4 wk = W[k];
+      const int4 rc = fs[wk.x], rx = fx[wk.x];
+      // the node's own right-hand side (its aggregated injection), then its step
+      const int xk = rc.x >> 4, mk = rc.z >= 0 ? 1 : rx.y;
+      const double2* xr = xall + size_t(a.W + warp) * a.nphi;  // staged right-hand sides
+      for (int i = 0; i < mk; ++i) x[xk + i] = xr[xk + i];
+      asm volatile("" ::: "memory");  // the step reads x through ld.shared asm
+      fwd_step(rc, rx);
+      asm volatile("" ::: "memory");
+      for (int i = 0; i < mk; ++i) a.tfwd[size_t(rhs) * a.nphi + xk + i] = x[xk + i];
+      const int up = wk.y >= 0 && W[wk.y].x >= 0 ? wk.y : -1;  // stop below kept nodes
+      if (sa <= sb) na = up;
+      if (sb <= sa) nb = up;
+    }
   }
+  __syncwarp();  // the walk (lane 0) wrote x
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
   const int4* bs = reinterpret_cast<const int4*>(M + a.bslot);
   const int4* bx = reinterpret_cast<const int4*>(M + a.bext);
   const int2* be = reinterpret_cast<const int2*>(M + a.bent);
-  rc = bs[lane];
-  rx = bx[lane];
+  int4 rc = bs[lane];
+  int4 rx = bx[lane];
   for (int br = 0; br < a.nbr; ++br) {
     const int4 nx = bs[(br + 1) * 32 + lane];
     const int4 nxx = bx[(br + 1) * 32 + lane];
@@ -589,6 +635,11 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   }
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
   for (int r = lane; r < a.nphi; r += 32) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
+  if (a.tdbg && blockIdx.x == 0 && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.tdbg[size_t(a.st->iter) * 8 + 5] = t;
+  }
 }
 
 // cfac[i] = (src >= 0 ? (src & 1 ? pinv : blocks)[src >> 1] : 0)

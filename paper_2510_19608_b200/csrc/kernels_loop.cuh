@@ -167,14 +167,32 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   }
 
   // ---- candidates: super-node edges, both directions, filtered ------------
+  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * 8 + 7] = globaltimer();
   if (tid == 0) s_cnt = 0;
   __syncthreads();
-  for (int b = tid; b < a.nb; b += kLoopThreads) {
-    const int x = a.sup[a.br_from[b]], y = a.sup[a.br_to[b]];
-    if (x == y) continue;
-    const unsigned mx = a.mask[x], my = a.mask[y];
-    if (y != a.slack && (my & ~mx) == 0u) keys[atomicAdd(&s_cnt, 1)] = (unsigned(x) << 16) | unsigned(y);
-    if (x != a.slack && (mx & ~my) == 0u) keys[atomicAdd(&s_cnt, 1)] = (unsigned(y) << 16) | unsigned(x);
+  // warp-aggregated slot allocation (one shared atomic per warp and direction)
+  for (int b0 = 0; b0 < a.nb; b0 += kLoopThreads) {
+    const int b = b0 + tid;
+    bool e1 = false, e2 = false;
+    unsigned k1 = 0, k2 = 0;
+    if (b < a.nb) {
+      const int x = a.sup[a.br_from[b]], y = a.sup[a.br_to[b]];
+      if (x != y) {
+        const unsigned mx = a.mask[x], my = a.mask[y];
+        e1 = y != a.slack && (my & ~mx) == 0u;
+        e2 = x != a.slack && (mx & ~my) == 0u;
+        k1 = (unsigned(x) << 16) | unsigned(y);
+        k2 = (unsigned(y) << 16) | unsigned(x);
+      }
+    }
+    const unsigned lane_lt = (1u << (tid & 31)) - 1u;
+    const unsigned m1 = __ballot_sync(0xffffffffu, e1), m2 = __ballot_sync(0xffffffffu, e2);
+    const int n1 = __popc(m1), n2 = __popc(m2);
+    int base = 0;
+    if ((tid & 31) == 0 && n1 + n2 > 0) base = atomicAdd(&s_cnt, n1 + n2);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (e1) keys[base + __popc(m1 & lane_lt)] = k1;
+    if (e2) keys[base + n1 + __popc(m2 & lane_lt)] = k2;
   }
   __syncthreads();
   const int C = s_cnt;
@@ -390,6 +408,8 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   if (tid == 0) {
     st->ns = ns - 1;
     st->iter = it + 1;
+    st->last_s = s;
+    st->last_r = r;
     if (a.has_target && double(a.n - (ns - 1)) / double(a.n) >= a.target) st->done = 1;
     if (it + 1 >= a.cap) st->done = 1;
     if (a.tdbg) a.tdbg[size_t(it) * 8 + 1] = globaltimer();
