@@ -50,9 +50,11 @@ def gen(case: str, **kw) -> Path:
     return d
 
 
-def reduce(d: Path, tag: str, *flags: str, radialize: bool = False) -> dict:
+def reduce(d: Path, tag: str, *flags: str, radialize: bool = False, reduced: bool = True) -> dict:
     args = ["reduce", "--net", str(d / "net.json"), "--scen", str(d / "scen.csv"),
-            "--trace-hex", str(d / f"trace_{tag}.txt"), "--reduced", str(d / f"reduced_{tag}.json"), *flags]
+            "--trace-hex", str(d / f"trace_{tag}.txt"), *flags]
+    if reduced:
+        args += ["--reduced", str(d / f"reduced_{tag}.json")]
     if radialize:
         args.append("--radialize")
     out = json.loads(run(*args))
@@ -81,9 +83,25 @@ def gz(path: Path) -> None:
     path.unlink()
 
 
+def large() -> None:
+    """BASELINE configs[2]/[3] shaped feeders (defaults, branching 0.3): the
+    5,991-node and 8,381-node synthetic feeders with 2 scenarios, and the
+    reference's first iterations (target = K/n; the CPU reference needs about
+    10 s per feeder for its serial column build)."""
+    for case, n, k in (("c3", 5991, 4), ("c4", 8381, 3)):
+        d = gen(case, n=n, seed=n, L=2, branching=0.3)
+        reduce(d, f"mag_3e-3_k{k}", "--e-bar", "3e-3", "--target", repr(k / n + 1e-12), "--workers", "0",
+               reduced=False)
+        for f in ["net.json", "scen.csv"]:
+            gz(d / f)
+
+
 def main() -> None:
     if not REF.exists():
         sys.exit("build oracle/_ref first: make -C oracle")
+    if sys.argv[1:] == ["large"]:
+        large()
+        return
     # C1: ~100-node acceptance-recipe feeder, 4 scenarios (BASELINE configs[0])
     d = gen("c1", n=100, seed=1000, L=4, preset="acceptance")
     for e in ["1e-4", "1e-3", "3e-3", "1e-2"]:

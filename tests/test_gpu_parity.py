@@ -218,3 +218,13 @@ def test_reload_reuses_context():
     assert [(t.s, t.r) for t in b.trace] == [(s, r) for s, r, *_ in rows]
     with pytest.raises(kr.ValidationError):
         ctx.reload(host("m40"))
+
+
+@pytest.mark.parametrize("case", ["c3", "c4"])
+def test_large_feeders_first_iterations_bitwise(case):
+    """BASELINE configs[2]/[3]-shaped feeders (5,991 and 8,381 nodes, 2
+    scenarios): the reference's first iterations and its final errors."""
+    (tag, meta), = runs(case).items()
+    ctx = kr.Context(host(case))
+    res = ctx.run_reduction(cfg_from_flags([f for f in meta["flags"] if f not in ("--workers", "0")]))
+    assert_trace(res, case, tag)
