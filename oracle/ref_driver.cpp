@@ -136,6 +136,7 @@ ReductionConfig make_cfg(const std::map<std::string, std::string>& a) {
   cfg.objective = gets(a, "objective", "mag") == "complex" ? Objective::complex_error
                                                             : Objective::magnitude;
   if (a.count("target")) cfg.target_reduction = getd(a, "target", 1.0);
+  if (a.count("use-delta")) cfg.use_delta = getl(a, "use-delta", 1) != 0;  // 0: eval_full_solve path
   long w = getl(a, "workers", 1);
   if (w <= 0) w = long(std::thread::hardware_concurrency());
   cfg.workers = int(w);

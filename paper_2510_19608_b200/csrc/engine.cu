@@ -77,6 +77,7 @@ struct DBuf {
 #include "kernels_score2.cuh"
 #include "kernels_score3.cuh"
 #include "kernels_loop.cuh"
+#include "kernels_naive.cuh"
 
 namespace kronred::b200 {
 namespace {
@@ -831,6 +832,7 @@ struct Engine::Impl {
     CK(cudaFuncSetAttribute(score3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 256));
     CK(cudaFuncSetAttribute(score_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(base_refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
+    CK(cudaFuncSetAttribute(naive_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     n = prob.y.n;
     prow_off.assign(size_t(n) + 1, 0);
@@ -958,7 +960,8 @@ struct Engine::Impl {
     if (c.target_reduction && !(*c.target_reduction >= 0 && *c.target_reduction <= 1))
       throw ConfigError("target_reduction must lie in [0,1]");
     if (L == 0) throw ValidationError("scenario library is empty");
-    if (!c.use_delta) throw ConfigError("use_delta=false (naive per-candidate solves) is not implemented yet");
+    if (!c.use_delta && full.bW <= 0)
+      throw ConfigError("use_delta=false needs the factor program in shared memory (network too large)");
     cfg = c;
     // AnchoredSolver (re-factorized per run, as run_reduction does, reduce.cpp:359)
     factorize(full, d_yin.p, pivot_floor, /*check_now=*/false);
@@ -984,6 +987,17 @@ struct Engine::Impl {
   // per-iteration inputs: super-node table + candidates (pinned, async)
   void upload_iteration(long long c0, long long c1) {
     const long long C = c1 - c0;
+    if (!cfg.use_delta) {
+      // full-solve path: candidate lists + super-node / member CSR
+      d_cs.alloc(size_t(2 * n) + 1);
+      d_cr.alloc(size_t(2 * n) + 1);
+      if (C > 0) {
+        CK(cudaMemcpyAsync(d_cs.p, cs.data() + c0, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_cr.p, cr.data() + c0, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
+      }
+      upload_members();
+      return;
+    }
     if (cfg.objective == Objective::magnitude) {
       // 4-row blocks that never split a super-node; inert padding rows
       // (phase field 3) fill each block
@@ -1052,22 +1066,72 @@ struct Engine::Impl {
     }
     if (C > 0) CK(cudaMemcpyAsync(d_cand.p, h_cand, size_t(C) * sizeof(int4), cudaMemcpyHostToDevice, stream));
     CK(cudaMemcpyAsync(d_snt.p, h_snt, size_t(k) * sizeof(unsigned), cudaMemcpyHostToDevice, stream));
-    if (cfg.objective == Objective::complex_error) {
-      std::vector<int> off(size_t(n) + 1, 0), lst;
-      for (int i = 0; i < n; ++i) {
-        for (int j : hs.members[size_t(i)]) lst.push_back(j);
-        off[size_t(i) + 1] = int(lst.size());
-      }
-      CK(cudaMemcpy(d_memoff.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
-      if (!lst.empty()) CK(cudaMemcpy(d_memlist.p, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(d_snid.p, hs.supernodes.data(), hs.supernodes.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (cfg.objective == Objective::complex_error) upload_members();
+  }
+
+  // members of every super-node (CSR by id) and the ascending super-node list
+  void upload_members() {
+    std::vector<int> off(size_t(n) + 1, 0), lst;
+    for (int i = 0; i < n; ++i) {
+      for (int j : hs.members[size_t(i)]) lst.push_back(j);
+      off[size_t(i) + 1] = int(lst.size());
     }
+    CK(cudaMemcpy(d_memoff.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (!lst.empty()) CK(cudaMemcpy(d_memlist.p, lst.data(), lst.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_snid.p, hs.supernodes.data(), hs.supernodes.size() * sizeof(int), cudaMemcpyHostToDevice));
+  }
+
+  // use_delta=false scorer (kernels_naive.cuh): one warp per (candidate, scenario)
+  void launch_naive(long long C) {
+    BaseArgs b = full.bprog;
+    b.L = L;
+    b.cfac = full.cfac.p;
+    b.meta = full.bmeta.p;
+    b.iaggp = d_iaggp.p;
+    b.kept_val = d_slackv.p;
+    const size_t fixed = size_t(b.ncf) * 16 + size_t(b.nmeta) * 4;
+    const size_t per_warp = size_t(nphi) * 16 + size_t(n) * 8;
+    int W = 0;
+    for (int w = 8; w >= 1; --w)
+      if (fixed + size_t(w) * per_warp <= size_t(optin_smem) - 64) {
+        W = w;
+        break;
+      }
+    if (W == 0) throw ConfigError("use_delta=false: the factor program does not fit in shared memory");
+    b.W = W;
+    NaiveArgs q{};
+    q.b = b;
+    q.C = int(C);
+    q.cs = d_cs.p;
+    q.cr = d_cr.p;
+    q.ns = int(hs.supernodes.size());
+    q.sn_id = d_snid.p;
+    q.mem_off = d_memoff.p;
+    q.mem_list = d_memlist.p;
+    q.mask = d_mask.p;
+    q.prow_off = d_prow_off.p;
+    q.vhat_full = d_vhat.p;
+    q.n = n;
+    q.e_bar = cfg.e_bar;
+    q.complex_obj = cfg.objective == Objective::complex_error ? 1 : 0;
+    q.out_sm = d_psmice.p;
+    q.out_mx = d_pmaxerr.p;
+    q.ldc = s3_ldc();
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const long long pairs = C * L;
+    const int grid = int(std::max<long long>(1, std::min<long long>((pairs + W - 1) / W, 4LL * sms)));
+    naive_score_kernel<<<grid, 32 * W, fixed + size_t(W) * per_warp, stream>>>(q);
+    launched();
+    CK(cudaGetLastError());
   }
 
   void launch_score(long long C) {
     if (C <= 0) return;
     if (profile) CK(cudaEventRecord(ev_a, stream));
-    if (cfg.objective == Objective::magnitude) {
+    if (!cfg.use_delta) {
+      launch_naive(C);
+    } else if (cfg.objective == Objective::magnitude) {
       RowArgs g{};
       g.L = L;
       g.nphi = nphi;
@@ -1224,8 +1288,11 @@ struct Engine::Impl {
     score_c0 = c0;
     upload_iteration(c0, c1);
     launch_score(C);
-    argmin_kernel<<<1, 1024, 0, stream>>>(int(std::max(C, 0LL)), L, (cfg.objective == Objective::magnitude && use_score3) ? s3_ldc() : 0, cfg.e_bar, c0, d_psmice.p, d_pmaxerr.p,
-                                          cfg.objective == Objective::magnitude ? d_pcand.p : nullptr,
+    const bool naive = !cfg.use_delta;
+    argmin_kernel<<<1, 1024, 0, stream>>>(int(std::max(C, 0LL)), L,
+                                          (naive || (cfg.objective == Objective::magnitude && use_score3)) ? s3_ldc() : 0,
+                                          cfg.e_bar, c0, d_psmice.p, d_pmaxerr.p,
+                                          (cfg.objective == Objective::magnitude && !naive) ? d_pcand.p : nullptr,
                                           d_best.p);
     launched();
     CK(cudaGetLastError());
@@ -1276,7 +1343,7 @@ struct Engine::Impl {
   size_t enum_smem() const { return pow2_at_least(std::max<size_t>(2 * prob.net.branches.size(), 1)) * sizeof(unsigned); }
 
   bool device_loop_ok(const ReductionConfig& c) const {
-    return !force_host_loop && c.objective == Objective::magnitude && world == 1 && !profile && use_tiles &&
+    return !force_host_loop && c.use_delta && c.objective == Objective::magnitude && world == 1 && !profile && use_tiles &&
            !use_seg && full.bW > 0 && n <= 65535 && enum_smem() + 24 * 1024 <= size_t(optin_smem);
   }
 
@@ -1759,11 +1826,11 @@ void Engine::loop_score_all(double* smice, std::uint8_t* feasible, double* max_e
   I.upload_iteration(0, C);
   I.launch_score(C);
   // score3 writes scenario-major [L][ldc]; the complex scorer candidate-major [C][L]
-  const bool tr = I.cfg.objective == Objective::magnitude && I.use_score3;
+  const bool tr = !I.cfg.use_delta || (I.cfg.objective == Objective::magnitude && I.use_score3);
   const size_t ldc = size_t(I.s3_ldc());
   const size_t npair = tr ? ldc * I.L : size_t(C) * I.L;
   std::vector<double> ps(npair), pm(npair), pc(static_cast<size_t>(C));
-  const bool mag = I.cfg.objective == Objective::magnitude && !I.use_score3;
+  const bool mag = I.cfg.use_delta && I.cfg.objective == Objective::magnitude && !I.use_score3;
   if (C > 0) {
     if (mag)
       CK(cudaMemcpyAsync(pc.data(), I.d_pcand.p, pc.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));

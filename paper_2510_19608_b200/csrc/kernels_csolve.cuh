@@ -426,154 +426,91 @@ __device__ __forceinline__ void sts2(unsigned addr, C2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }
 
-__global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
-  extern __shared__ __align__(16) double2 smem[];
-  __shared__ unsigned long long bar;
-  if (a.st && a.st->done) return;
-  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    a.tdbg[size_t(a.st->iter) * 8 + 4] = t;
-  }
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rhs = blockIdx.x * a.W + warp;
-  const int nw = min(a.W, a.L - blockIdx.x * a.W);
-  double2* cf = smem;
-  int* M = reinterpret_cast<int*>(cf + a.ncf);
-  double2* xall = reinterpret_cast<double2*>(M + a.nmeta);
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // incremental: x <- last forward values, and the right-hand sides of the
-    // re-eliminated path nodes come from a second buffer (both TMA-staged)
-    const unsigned per = unsigned(a.nphi) * 16u;
-    const unsigned bytes = unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u + unsigned(nw) * per * (a.inc ? 2u : 1u);
-    mbar_expect_tx(&bar, bytes);
-    if (a.ncf) bulk_g2s(cf, a.cfac, unsigned(a.ncf) * 16u, &bar);
-    bulk_g2s(M, a.meta, unsigned(a.nmeta) * 4u, &bar);
-    const double2* src = a.inc ? a.tfwd : a.iaggp;
-    for (int w = 0; w < nw; ++w)
-      bulk_g2s(xall + size_t(w) * a.nphi, src + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
-    if (a.inc)
-      for (int w = 0; w < nw; ++w)
-        bulk_g2s(xall + size_t(a.W + w) * a.nphi, a.iaggp + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
-  }
-  __syncthreads();
-  mbar_wait(&bar, 0);
-  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[0] = clock64();
-  if (warp >= nw) return;
-  double2* x = xall + size_t(warp) * a.nphi;
-  for (int k = lane; k < a.nkept; k += 32) {
-    const int xe = M[a.kept + 2 * k], ki = M[a.kept + 2 * k + 1];
-    const int x0 = xe & 0xffffff, m = xe >> 24;
-    for (int i = 0; i < m; ++i) x[x0 + i] = a.kept_val[ki * 3 + i];
-  }
-  __syncwarp();
-  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[1] = clock64();
-  // records: int4 {x_k*16 (<0: empty), pinv*16, x_j0*16, block0*16} (byte
-  // offsets into x / cf) + int4 {general?, m_k, first extra entry, extra count}.
-  // Scalar steps (one present phase, single-phase pulls) run one straight-line
-  // sequence on 32-bit shared addresses; the record arrays carry one padding
-  // round so the prefetch of round i+1 is unconditional.
-  const unsigned xs = unsigned(__cvta_generic_to_shared(x)), cs = unsigned(__cvta_generic_to_shared(cf));
-  const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
-  const int4* fx = reinterpret_cast<const int4*>(M + a.fext);
-  const int2* fe = reinterpret_cast<const int2*>(M + a.fent);
-  auto fwd_step = [&](const int4 rc, const int4 rx) {
-    if (rc.x >= 0 && rc.z >= 0) {
-        // scalar step: two pulls inline (zero pulls when absent), their
-        // products in flight together; the subtractions keep elimination order
-        const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y);
-        const C2 t1 = lds2(xs + rx.x), a1 = lds2(cs + rx.y);
-        const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
-        const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
-        C2 b = dev::csub(dev::csub(b0, u0), u1);
-        int e = rx.z;
-        const int e_end = rx.z + rx.w;
+// One forward elimination step of the lane-slot program (pull form): node k's
+// right-hand side minus its children's contributions in elimination order,
+// times pinv_k (solver.cpp:125-134; the scalar fast path and the general
+// 3x3 path).
+__device__ __forceinline__ void tree_fwd_step(const int4 rc, const int4 rx, unsigned xs, unsigned cs, double2* x,
+                                              const double2* cf, const int2* fe) {
+  if (rc.x >= 0 && rc.z >= 0) {
+      // scalar step: two pulls inline (zero pulls when absent), their
+      // products in flight together; the subtractions keep elimination order
+      const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y);
+      const C2 t1 = lds2(xs + rx.x), a1 = lds2(cs + rx.y);
+      const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
+      const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
+      C2 b = dev::csub(dev::csub(b0, u0), u1);
+      int e = rx.z;
+      const int e_end = rx.z + rx.w;
 #pragma unroll 1
-        for (; e < e_end; e += 3) {  // further children, predicated batches of three
-          C2 u[3];
+      for (; e < e_end; e += 3) {  // further children, predicated batches of three
+        C2 u[3];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            const int2 en = fe[min(e + q, e_end - 1)];
-            u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
-          }
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            if (e + q < e_end) b = dev::csub(b, u[q]);
+        for (int q = 0; q < 3; ++q) {
+          const int2 en = fe[min(e + q, e_end - 1)];
+          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
         }
-        sts2(xs + rc.x, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, b)));
-      } else if (rc.x >= 0) {
-        const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
-        C2 b[3];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) b[i] = i < mk ? ld2(x + xk + i) : C2{0.0, 0.0};
-        for (int e = rx.z; e < rx.z + rx.w; ++e) {
-          const int2 en = fe[e];
-          const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
-          C2 tj[3];
+        for (int q = 0; q < 3; ++q)
+          if (e + q < e_end) b = dev::csub(b, u[q]);
+      }
+      sts2(xs + rc.x, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, b)));
+    } else if (rc.x >= 0) {
+      const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
+      C2 b[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) tj[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
+      for (int i = 0; i < 3; ++i) b[i] = i < mk ? ld2(x + xk + i) : C2{0.0, 0.0};
+      for (int e = rx.z; e < rx.z + rx.w; ++e) {
+        const int2 en = fe[e];
+        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+        C2 tj[3];
 #pragma unroll
-          for (int r = 0; r < 3; ++r) {
-            if (r >= mk) continue;
-            C2 acc = {0.0, 0.0};
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-              if (c < mj) acc = dev::cadd(acc, dev::cmul(ld2(cf + bo + r * mj + c), tj[c]));
-            b[r] = dev::csub(b[r], acc);
-          }
-        }
+        for (int c = 0; c < 3; ++c) tj[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
           if (r >= mk) continue;
           C2 acc = {0.0, 0.0};
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            if (c < mk) acc = dev::cadd(acc, dev::cmul(ld2(cf + po + r * mk + c), b[c]));
-          st2(x + xk + r, acc);
+            if (c < mj) acc = dev::cadd(acc, dev::cmul(ld2(cf + bo + r * mj + c), tj[c]));
+          b[r] = dev::csub(b[r], acc);
         }
       }
-  };
-  if (!a.inc) {
-    int4 rc = fs[lane];
-    int4 rx = fx[lane];
-    for (int fr = 0; fr < a.nfr; ++fr) {
-      const int4 nx = fs[(fr + 1) * 32 + lane];
-      const int4 nxx = fx[(fr + 1) * 32 + lane];
-      fwd_step(rc, rx);
-      rc = nx;
-      rx = nxx;
-      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (r >= mk) continue;
+        C2 acc = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          if (c < mk) acc = dev::cadd(acc, dev::cmul(ld2(cf + po + r * mk + c), b[c]));
+        st2(x + xk + r, acc);
+      }
     }
-    if (a.tfwd)  // keep the forward values for the next (incremental) refresh
-      for (int r = lane; r < a.nphi; r += 32) a.tfwd[size_t(rhs) * a.nphi + r] = x[r];
-  } else if (lane == 0) {
-    // walk the ancestors of the two changed nodes in elimination order
-    const int4* W = reinterpret_cast<const int4*>(M + a.walk);
-    int na = a.st ? a.st->last_s : a.inc_s, nb = a.st ? a.st->last_r : a.inc_r;
-    if (na >= 0 && W[na].x < 0) na = -1;  // kept (slack): no forward step
-    if (nb >= 0 && W[nb].x < 0) nb = -1;
-    while (na >= 0 || nb >= 0) {
-      const int sa = na >= 0 ? W[na].z : 0x7fffffff, sb = nb >= 0 ? W[nb].z : 0x7fffffff;
-      const int k = sa <= sb ? na : nb;
-      const int4 wk = W[k];
-      const int4 rc = fs[wk.x], rx = fx[wk.x];
-      // the node's own right-hand side (its aggregated injection), then its step
-      const int xk = rc.x >> 4, mk = rc.z >= 0 ? 1 : rx.y;
-      const double2* xr = xall + size_t(a.W + warp) * a.nphi;  // staged right-hand sides
-      for (int i = 0; i < mk; ++i) x[xk + i] = xr[xk + i];
-      asm volatile("" ::: "memory");  // the step reads x through ld.shared asm
-      fwd_step(rc, rx);
-      asm volatile("" ::: "memory");
-      for (int i = 0; i < mk; ++i) a.tfwd[size_t(rhs) * a.nphi + xk + i] = x[xk + i];
-      const int up = wk.y >= 0 && W[wk.y].x >= 0 ? wk.y : -1;  // stop below kept nodes
-      if (sa <= sb) na = up;
-      if (sb <= sa) nb = up;
-    }
+}
+
+// Full forward sweep of the lane-slot program, one level per round.
+__device__ __forceinline__ void tree_forward(const BaseArgs& a, const int* M, unsigned xs, unsigned cs, double2* x,
+                                             const double2* cf, int lane) {
+  const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
+  const int4* fx = reinterpret_cast<const int4*>(M + a.fext);
+  const int2* fe = reinterpret_cast<const int2*>(M + a.fent);
+  int4 rc = fs[lane];
+  int4 rx = fx[lane];
+  for (int fr = 0; fr < a.nfr; ++fr) {
+    const int4 nx = fs[(fr + 1) * 32 + lane];
+    const int4 nxx = fx[(fr + 1) * 32 + lane];
+    tree_fwd_step(rc, rx, xs, cs, x, cf, fe);
+    rc = nx;
+    rx = nxx;
+    __syncwarp();
   }
-  __syncwarp();  // the walk (lane 0) wrote x
-  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
+}
+
+// Backward sweep of the lane-slot program (solver.cpp:136-147): every
+// eliminated node resolved against its (already final) couplings, one level
+// per round.
+__device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, unsigned xs, unsigned cs, double2* x,
+                                              const double2* cf, int lane) {
   const int4* bs = reinterpret_cast<const int4*>(M + a.bslot);
   const int4* bx = reinterpret_cast<const int4*>(M + a.bext);
   const int2* be = reinterpret_cast<const int2*>(M + a.bent);
@@ -633,6 +570,92 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     rx = nxx;
     __syncwarp();
   }
+}
+
+__global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ unsigned long long bar;
+  if (a.st && a.st->done) return;
+  if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.tdbg[size_t(a.st->iter) * 8 + 4] = t;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rhs = blockIdx.x * a.W + warp;
+  const int nw = min(a.W, a.L - blockIdx.x * a.W);
+  double2* cf = smem;
+  int* M = reinterpret_cast<int*>(cf + a.ncf);
+  double2* xall = reinterpret_cast<double2*>(M + a.nmeta);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // incremental: x <- last forward values, and the right-hand sides of the
+    // re-eliminated path nodes come from a second buffer (both TMA-staged)
+    const unsigned per = unsigned(a.nphi) * 16u;
+    const unsigned bytes = unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u + unsigned(nw) * per * (a.inc ? 2u : 1u);
+    mbar_expect_tx(&bar, bytes);
+    if (a.ncf) bulk_g2s(cf, a.cfac, unsigned(a.ncf) * 16u, &bar);
+    bulk_g2s(M, a.meta, unsigned(a.nmeta) * 4u, &bar);
+    const double2* src = a.inc ? a.tfwd : a.iaggp;
+    for (int w = 0; w < nw; ++w)
+      bulk_g2s(xall + size_t(w) * a.nphi, src + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
+    if (a.inc)
+      for (int w = 0; w < nw; ++w)
+        bulk_g2s(xall + size_t(a.W + w) * a.nphi, a.iaggp + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[0] = clock64();
+  if (warp >= nw) return;
+  double2* x = xall + size_t(warp) * a.nphi;
+  for (int k = lane; k < a.nkept; k += 32) {
+    const int xe = M[a.kept + 2 * k], ki = M[a.kept + 2 * k + 1];
+    const int x0 = xe & 0xffffff, m = xe >> 24;
+    for (int i = 0; i < m; ++i) x[x0 + i] = a.kept_val[ki * 3 + i];
+  }
+  __syncwarp();
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[1] = clock64();
+  // records: int4 {x_k*16 (<0: empty), pinv*16, x_j0*16, block0*16} (byte
+  // offsets into x / cf) + int4 {general?, m_k, first extra entry, extra count}.
+  // Scalar steps (one present phase, single-phase pulls) run one straight-line
+  // sequence on 32-bit shared addresses; the record arrays carry one padding
+  // round so the prefetch of round i+1 is unconditional.
+  const unsigned xs = unsigned(__cvta_generic_to_shared(x)), cs = unsigned(__cvta_generic_to_shared(cf));
+  const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
+  const int4* fx = reinterpret_cast<const int4*>(M + a.fext);
+  const int2* fe = reinterpret_cast<const int2*>(M + a.fent);
+  if (!a.inc) {
+    tree_forward(a, M, xs, cs, x, cf, lane);
+    if (a.tfwd)  // keep the forward values for the next (incremental) refresh
+      for (int r = lane; r < a.nphi; r += 32) a.tfwd[size_t(rhs) * a.nphi + r] = x[r];
+  } else if (lane == 0) {
+    // walk the ancestors of the two changed nodes in elimination order
+    const int4* W = reinterpret_cast<const int4*>(M + a.walk);
+    int na = a.st ? a.st->last_s : a.inc_s, nb = a.st ? a.st->last_r : a.inc_r;
+    if (na >= 0 && W[na].x < 0) na = -1;  // kept (slack): no forward step
+    if (nb >= 0 && W[nb].x < 0) nb = -1;
+    while (na >= 0 || nb >= 0) {
+      const int sa = na >= 0 ? W[na].z : 0x7fffffff, sb = nb >= 0 ? W[nb].z : 0x7fffffff;
+      const int k = sa <= sb ? na : nb;
+      const int4 wk = W[k];
+      const int4 rc = fs[wk.x], rx = fx[wk.x];
+      // the node's own right-hand side (its aggregated injection), then its step
+      const int xk = rc.x >> 4, mk = rc.z >= 0 ? 1 : rx.y;
+      const double2* xr = xall + size_t(a.W + warp) * a.nphi;  // staged right-hand sides
+      for (int i = 0; i < mk; ++i) x[xk + i] = xr[xk + i];
+      asm volatile("" ::: "memory");  // the step reads x through ld.shared asm
+      tree_fwd_step(rc, rx, xs, cs, x, cf, fe);
+      asm volatile("" ::: "memory");
+      for (int i = 0; i < mk; ++i) a.tfwd[size_t(rhs) * a.nphi + xk + i] = x[xk + i];
+      const int up = wk.y >= 0 && W[wk.y].x >= 0 ? wk.y : -1;  // stop below kept nodes
+      if (sa <= sb) na = up;
+      if (sb <= sa) nb = up;
+    }
+  }
+  __syncwarp();  // the walk (lane 0) wrote x
+  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
+  tree_backward(a, M, xs, cs, x, cf, lane);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
   for (int r = lane; r < a.nphi; r += 32) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
   if (a.tdbg && blockIdx.x == 0 && tid == 0) {

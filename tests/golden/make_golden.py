@@ -96,11 +96,23 @@ def large() -> None:
             gz(d / f)
 
 
+def naive() -> None:
+    """use_delta = false (eval_full_solve, reduce.cpp:132-167) on the small
+    feeders: its full solves round differently from the delta path."""
+    reduce(HERE / "c1", "naive_mag_1e-3", "--e-bar", "1e-3", "--use-delta", "0")
+    reduce(HERE / "c1", "naive_complex_1e-3", "--e-bar", "1e-3", "--objective", "complex", "--use-delta", "0")
+    reduce(HERE / "m40", "naive_mag_1e-3", "--e-bar", "1e-3", "--use-delta", "0")
+    reduce(HERE / "s24", "naive_mag_5e-4", "--e-bar", "5e-4", "--use-delta", "0")
+
+
 def main() -> None:
     if not REF.exists():
         sys.exit("build oracle/_ref first: make -C oracle")
     if sys.argv[1:] == ["large"]:
         large()
+        return
+    if sys.argv[1:] == ["naive"]:
+        naive()
         return
     # C1: ~100-node acceptance-recipe feeder, 4 scenarios (BASELINE configs[0])
     d = gen("c1", n=100, seed=1000, L=4, preset="acceptance")

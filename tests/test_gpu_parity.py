@@ -32,6 +32,8 @@ def cfg_from_flags(flags: list[str]) -> kr.ReductionConfig:
             c.objective = v
         elif f == "--target":
             c.target_reduction = float(v)
+        elif f == "--use-delta":
+            c.use_delta = v != "0"
     return c
 
 
