@@ -134,6 +134,7 @@ struct DevElim {
   BaseArgs bprog{};
   DBuf<int> bmeta;
   int bW = 0, bsmem = 0;
+  bool bsm = true;  // factor + program staged in shared memory (else read from global)
   const int* P(int which) const { return ints.p + off[size_t(which)]; }
 };
 
@@ -581,14 +582,33 @@ struct Engine::Impl {
       CK(cudaMemcpyAsync(d.bmeta.p, bm.data(), bm.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
       const size_t fixed = size_t(B.ncf) * 16 + size_t(B.nmeta) * 4;
       d.bW = 0;
+      d.bsm = true;
+      B.rhs_staged = B.walk >= 0 ? 1 : 0;
       // two nph-row buffers per warp when the incremental walk is available
-      const size_t per_warp = size_t(nph) * 16 * (B.walk >= 0 ? 2 : 1);
+      size_t per_warp = size_t(nph) * 16 * (B.walk >= 0 ? 2 : 1);
       for (int w = 8; w >= 1; --w)
         if (fixed + size_t(w) * per_warp <= size_t(optin_smem) - 64) {
           d.bW = w;
           break;
         }
-      d.bsmem = int(fixed + size_t(std::max(d.bW, 1)) * per_warp);
+      size_t fx = fixed;
+      if (d.bW == 0) {
+        // large network: factor and program stay in global memory (read
+        // through L1/L2); only the solution (and, if they fit, the staged
+        // right-hand sides) live in shared memory
+        d.bsm = false;
+        fx = 0;
+        for (int stage = 1; stage >= 0 && d.bW == 0; --stage) {
+          per_warp = size_t(nph) * 16 * (B.walk >= 0 && stage ? 2 : 1);
+          for (int w = 8; w >= 1; --w)
+            if (size_t(w) * per_warp <= size_t(optin_smem) - 64) {
+              d.bW = w;
+              B.rhs_staged = B.walk >= 0 && stage ? 1 : 0;
+              break;
+            }
+        }
+      }
+      d.bsmem = int(fx + size_t(std::max(d.bW, 1)) * per_warp);
     }
     d.meta.alloc(meta.size());
     if (!meta.empty())
@@ -772,7 +792,10 @@ struct Engine::Impl {
       b.inc_s = s;
       b.inc_r = r;
       if (profile) CK(cudaEventRecord(ev_a, stream));
-      base_refresh_kernel<<<(L + b.W - 1) / b.W, 32 * b.W, full.bsmem, stream>>>(b);
+      if (full.bsm)
+        base_refresh_kernel<true><<<(L + b.W - 1) / b.W, 32 * b.W, full.bsmem, stream>>>(b);
+      else
+        base_refresh_kernel<false><<<(L + b.W - 1) / b.W, 32 * b.W, full.bsmem, stream>>>(b);
       launched();
       CK(cudaGetLastError());
       if (profile) {
@@ -831,7 +854,8 @@ struct Engine::Impl {
     CK(cudaFuncSetAttribute(score2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 256));
     CK(cudaFuncSetAttribute(score_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
-    CK(cudaFuncSetAttribute(base_refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
+    CK(cudaFuncSetAttribute(base_refresh_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
+    CK(cudaFuncSetAttribute(base_refresh_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(naive_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     n = prob.y.n;
@@ -960,7 +984,7 @@ struct Engine::Impl {
     if (c.target_reduction && !(*c.target_reduction >= 0 && *c.target_reduction <= 1))
       throw ConfigError("target_reduction must lie in [0,1]");
     if (L == 0) throw ValidationError("scenario library is empty");
-    if (!c.use_delta && full.bW <= 0)
+    if (!c.use_delta && (full.bW <= 0 || !full.bsm))
       throw ConfigError("use_delta=false needs the factor program in shared memory (network too large)");
     cfg = c;
     // AnchoredSolver (re-factorized per run, as run_reduction does, reduce.cpp:359)
@@ -1537,7 +1561,10 @@ struct Engine::Impl {
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
       enum_kernel<<<1, kLoopThreads, enum_smem(), stream2>>>(lb);
-      base_refresh_kernel<<<(L + bb.W - 1) / bb.W, 32 * bb.W, full.bsmem, stream>>>(bb);
+      if (full.bsm)
+        base_refresh_kernel<true><<<(L + bb.W - 1) / bb.W, 32 * bb.W, full.bsmem, stream>>>(bb);
+      else
+        base_refresh_kernel<false><<<(L + bb.W - 1) / bb.W, 32 * bb.W, full.bsmem, stream>>>(bb);
       CK(cudaEventRecord(ev_join, stream2));
       CK(cudaStreamWaitEvent(stream, ev_join, 0));
       }

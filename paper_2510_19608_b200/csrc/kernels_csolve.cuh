@@ -391,6 +391,7 @@ struct BaseArgs {
   int inc;                // 1: incremental (s, r below or st->last_s/last_r), 0: full sweep
   int inc_s, inc_r;       // changed nodes (host-driven loop)
   int walk;               // ints offset in M of [node] int4 {record, parent, step, 0} (-1 record: kept)
+  int rhs_staged;         // incremental: right-hand sides staged in a second buffer per warp
 };
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -426,17 +427,30 @@ __device__ __forceinline__ void sts2(unsigned addr, C2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// Factor coefficient at a byte offset: shared memory (32-bit address) when
+// the program is staged, global (read-only path) otherwise.
+template <bool SM>
+__device__ __forceinline__ C2 cfl(unsigned cs, const double2* cf, int byteoff) {
+  if constexpr (SM) {
+    return lds2(cs + unsigned(byteoff));
+  } else {
+    const double2 v = __ldg(cf + (byteoff >> 4));
+    return {v.x, v.y};
+  }
+}
+
 // One forward elimination step of the lane-slot program (pull form): node k's
 // right-hand side minus its children's contributions in elimination order,
 // times pinv_k (solver.cpp:125-134; the scalar fast path and the general
 // 3x3 path).
+template <bool SM>
 __device__ __forceinline__ void tree_fwd_step(const int4 rc, const int4 rx, unsigned xs, unsigned cs, double2* x,
                                               const double2* cf, const int2* fe) {
   if (rc.x >= 0 && rc.z >= 0) {
       // scalar step: two pulls inline (zero pulls when absent), their
       // products in flight together; the subtractions keep elimination order
-      const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y);
-      const C2 t1 = lds2(xs + rx.x), a1 = lds2(cs + rx.y);
+      const C2 b0 = lds2(xs + rc.x), tj = lds2(xs + rc.z), aa = cfl<SM>(cs, cf, rc.w), pv = cfl<SM>(cs, cf, rc.y);
+      const C2 t1 = lds2(xs + rx.x), a1 = cfl<SM>(cs, cf, rx.y);
       const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
       const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
       C2 b = dev::csub(dev::csub(b0, u0), u1);
@@ -448,7 +462,7 @@ __device__ __forceinline__ void tree_fwd_step(const int4 rc, const int4 rx, unsi
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           const int2 en = fe[min(e + q, e_end - 1)];
-          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
+          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(cfl<SM>(cs, cf, en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
         }
 #pragma unroll
         for (int q = 0; q < 3; ++q)
@@ -489,6 +503,7 @@ __device__ __forceinline__ void tree_fwd_step(const int4 rc, const int4 rx, unsi
 }
 
 // Full forward sweep of the lane-slot program, one level per round.
+template <bool SM>
 __device__ __forceinline__ void tree_forward(const BaseArgs& a, const int* M, unsigned xs, unsigned cs, double2* x,
                                              const double2* cf, int lane) {
   const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
@@ -499,7 +514,7 @@ __device__ __forceinline__ void tree_forward(const BaseArgs& a, const int* M, un
   for (int fr = 0; fr < a.nfr; ++fr) {
     const int4 nx = fs[(fr + 1) * 32 + lane];
     const int4 nxx = fx[(fr + 1) * 32 + lane];
-    tree_fwd_step(rc, rx, xs, cs, x, cf, fe);
+    tree_fwd_step<SM>(rc, rx, xs, cs, x, cf, fe);
     rc = nx;
     rx = nxx;
     __syncwarp();
@@ -509,6 +524,7 @@ __device__ __forceinline__ void tree_forward(const BaseArgs& a, const int* M, un
 // Backward sweep of the lane-slot program (solver.cpp:136-147): every
 // eliminated node resolved against its (already final) couplings, one level
 // per round.
+template <bool SM>
 __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, unsigned xs, unsigned cs, double2* x,
                                               const double2* cf, int lane) {
   const int4* bs = reinterpret_cast<const int4*>(M + a.bslot);
@@ -520,7 +536,7 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
     const int4 nx = bs[(br + 1) * 32 + lane];
     const int4 nxx = bx[(br + 1) * 32 + lane];
     if (rc.x >= 0 && rx.x == 0) {
-      const C2 xj = lds2(xs + rc.z), aa = lds2(cs + rc.w), pv = lds2(cs + rc.y), t = lds2(xs + rc.x);
+      const C2 xj = lds2(xs + rc.z), aa = cfl<SM>(cs, cf, rc.w), pv = cfl<SM>(cs, cf, rc.y), t = lds2(xs + rc.x);
       C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj)));
       int e = rx.z;
       const int e_end = rx.z + rx.w;
@@ -530,7 +546,7 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           const int2 en = be[min(e + q, e_end - 1)];
-          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(lds2(cs + en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
+          u[q] = dev::cadd(C2{0.0, 0.0}, dev::cmul(cfl<SM>(cs, cf, en.y * 16), lds2(xs + (en.x & 0xffffff) * 16)));
         }
 #pragma unroll
         for (int q = 0; q < 3; ++q)
@@ -572,6 +588,10 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   }
 }
 
+// SM: factor and program staged in shared memory (TMA); otherwise they are
+// read from global memory (large networks) and only the solution vectors
+// are staged.
+template <bool SM>
 __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   __shared__ unsigned long long bar;
@@ -584,23 +604,27 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rhs = blockIdx.x * a.W + warp;
   const int nw = min(a.W, a.L - blockIdx.x * a.W);
-  double2* cf = smem;
-  int* M = reinterpret_cast<int*>(cf + a.ncf);
-  double2* xall = reinterpret_cast<double2*>(M + a.nmeta);
+  const double2* cf = SM ? smem : a.cfac;
+  const int* M = SM ? reinterpret_cast<const int*>(smem + a.ncf) : a.meta;
+  double2* xall = SM ? reinterpret_cast<double2*>(reinterpret_cast<int*>(smem + a.ncf) + a.nmeta) : smem;
+  const bool stage_rhs = a.inc && a.rhs_staged;
   if (tid == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // incremental: x <- last forward values, and the right-hand sides of the
-    // re-eliminated path nodes come from a second buffer (both TMA-staged)
+    // re-eliminated path nodes from a second buffer (both TMA-staged)
     const unsigned per = unsigned(a.nphi) * 16u;
-    const unsigned bytes = unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u + unsigned(nw) * per * (a.inc ? 2u : 1u);
+    const unsigned bytes = (SM ? unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u : 0u) +
+                           unsigned(nw) * per * (stage_rhs ? 2u : 1u);
     mbar_expect_tx(&bar, bytes);
-    if (a.ncf) bulk_g2s(cf, a.cfac, unsigned(a.ncf) * 16u, &bar);
-    bulk_g2s(M, a.meta, unsigned(a.nmeta) * 4u, &bar);
+    if (SM) {
+      if (a.ncf) bulk_g2s(smem, a.cfac, unsigned(a.ncf) * 16u, &bar);
+      bulk_g2s(reinterpret_cast<int*>(smem + a.ncf), a.meta, unsigned(a.nmeta) * 4u, &bar);
+    }
     const double2* src = a.inc ? a.tfwd : a.iaggp;
     for (int w = 0; w < nw; ++w)
       bulk_g2s(xall + size_t(w) * a.nphi, src + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
-    if (a.inc)
+    if (stage_rhs)
       for (int w = 0; w < nw; ++w)
         bulk_g2s(xall + size_t(a.W + w) * a.nphi, a.iaggp + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
   }
@@ -621,12 +645,13 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   // Scalar steps (one present phase, single-phase pulls) run one straight-line
   // sequence on 32-bit shared addresses; the record arrays carry one padding
   // round so the prefetch of round i+1 is unconditional.
-  const unsigned xs = unsigned(__cvta_generic_to_shared(x)), cs = unsigned(__cvta_generic_to_shared(cf));
+  const unsigned xs = unsigned(__cvta_generic_to_shared(x));
+  const unsigned cs = SM ? unsigned(__cvta_generic_to_shared(cf)) : 0u;
   const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
   const int4* fx = reinterpret_cast<const int4*>(M + a.fext);
   const int2* fe = reinterpret_cast<const int2*>(M + a.fent);
   if (!a.inc) {
-    tree_forward(a, M, xs, cs, x, cf, lane);
+    tree_forward<SM>(a, M, xs, cs, x, cf, lane);
     if (a.tfwd)  // keep the forward values for the next (incremental) refresh
       for (int r = lane; r < a.nphi; r += 32) a.tfwd[size_t(rhs) * a.nphi + r] = x[r];
   } else if (lane == 0) {
@@ -642,10 +667,10 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
       const int4 rc = fs[wk.x], rx = fx[wk.x];
       // the node's own right-hand side (its aggregated injection), then its step
       const int xk = rc.x >> 4, mk = rc.z >= 0 ? 1 : rx.y;
-      const double2* xr = xall + size_t(a.W + warp) * a.nphi;  // staged right-hand sides
+      const double2* xr = stage_rhs ? xall + size_t(a.W + warp) * a.nphi : a.iaggp + size_t(rhs) * a.nphi;
       for (int i = 0; i < mk; ++i) x[xk + i] = xr[xk + i];
       asm volatile("" ::: "memory");  // the step reads x through ld.shared asm
-      tree_fwd_step(rc, rx, xs, cs, x, cf, fe);
+      tree_fwd_step<SM>(rc, rx, xs, cs, x, cf, fe);
       asm volatile("" ::: "memory");
       for (int i = 0; i < mk; ++i) a.tfwd[size_t(rhs) * a.nphi + xk + i] = x[xk + i];
       const int up = wk.y >= 0 && W[wk.y].x >= 0 ? wk.y : -1;  // stop below kept nodes
@@ -655,7 +680,7 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   }
   __syncwarp();  // the walk (lane 0) wrote x
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
-  tree_backward(a, M, xs, cs, x, cf, lane);
+  tree_backward<SM>(a, M, xs, cs, x, cf, lane);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
   for (int r = lane; r < a.nphi; r += 32) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
   if (a.tdbg && blockIdx.x == 0 && tid == 0) {

@@ -85,9 +85,9 @@ __global__ void __launch_bounds__(256) naive_score_kernel(NaiveArgs a) {
     }
     __syncwarp();
     asm volatile("" ::: "memory");
-    tree_forward(B, M, xs, cs, x, cf, lane);
+    tree_forward<true>(B, M, xs, cs, x, cf, lane);
     __syncwarp();
-    tree_backward(B, M, xs, cs, x, cf, lane);
+    tree_backward<true>(B, M, xs, cs, x, cf, lane);
     __syncwarp();
     asm volatile("" ::: "memory");
     // score_scenario (reduce.cpp:89-123): per super-node i != r, the cluster
