@@ -74,7 +74,6 @@ struct DBuf {
 #include "kernels_elim.cuh"
 #include "kernels_csolve.cuh"
 #include "kernels_score.cuh"
-#include "kernels_score2.cuh"
 #include "kernels_score3.cuh"
 #include "kernels_loop.cuh"
 #include "kernels_naive.cuh"
@@ -187,10 +186,6 @@ struct Engine::Impl {
   DevElim kron_e, merr_e;
   DBuf<double2> merr_yin, merr_rhs, merr_out, merr_kv;
   DBuf<int> d_grpdone;  // score3 slice-completion counters
-  bool use_tiles = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) != "rows";
-  // score2 (kernels_score2.cuh) is the default; KRONRED_SCORER=tiles|seg|rows select the older variants
-  bool use_score3 = std::getenv("KRONRED_SCORER") == nullptr || std::string(std::getenv("KRONRED_SCORER")) == "score3";
-  bool use_score2 = std::getenv("KRONRED_SCORER") != nullptr && std::string(std::getenv("KRONRED_SCORER")) == "score2";
   // score3 geometry: 16 Z-column slots per CTA, scenario slices of up to 8
   static constexpr int kS3Slots = 16;
   int s3_ls() const { return std::min(L, 8); }
@@ -221,7 +216,6 @@ struct Engine::Impl {
     q.tplain = d_tplain.p;
     return q;
   }
-  bool use_seg = std::getenv("KRONRED_SCORER") != nullptr && std::string(std::getenv("KRONRED_SCORER")) == "seg";
 
   // threads per scorer CTA: a multiple of L (whole candidates) and of 32
   int score_cta_threads() const {
@@ -850,14 +844,10 @@ struct Engine::Impl {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     for (auto fn : {score_kernel<false>, score_kernel<true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
-    CK(cudaFuncSetAttribute(score_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
-    CK(cudaFuncSetAttribute(score2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(score3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 256));
-    CK(cudaFuncSetAttribute(score_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     CK(cudaFuncSetAttribute(base_refresh_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(base_refresh_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(naive_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
-    CK(cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     n = prob.y.n;
     prow_off.assign(size_t(n) + 1, 0);
     for (int i = 0; i < n; ++i) {
@@ -1156,102 +1146,19 @@ struct Engine::Impl {
     if (!cfg.use_delta) {
       launch_naive(C);
     } else if (cfg.objective == Objective::magnitude) {
-      RowArgs g{};
-      g.L = L;
-      g.nphi = nphi;
-      g.R = R;
-      g.tab = d_tab.p;
-      g.mask = d_mask.p;
-      g.prow_off = d_prow_off.p;
-      g.Z = d_Z.p;
-      g.bv = d_bv.p;
-      g.iagg = d_iagg.p;
-      g.out_smice = d_psmice.p;
-      g.out_maxerr = d_pmaxerr.p;
-      const int P = score_cta_threads();
-      const int G = (P % L == 0) ? P / L : 1;
-      const long long pairs = C * L;
-      int S = int(std::min<long long>(std::max<long long>(1, (148LL * 1024 + pairs - 1) / std::max(1LL, pairs)),
-                                      std::max(1, 512 / P)));
-      S = std::min(S, 16);
-      g.S = S;
-      g.G = G;
-      g.cand = d_cand.p;
-      g.cand_idx = d_cidx.p;
-      g.out_cand = d_pcand.p;
-      g.e_bar = cfg.e_bar;
-      g.C = int(C);
-      int ctas = 0;
+      // score3 (kernels_score3.cuh): work items = candidate group x scenario slice
+      S3Args q = s3_args();
+      q.C = int(C);
+      q.R = R;
+      int c3 = 0;
       for (int k = 1; k <= 3; ++k) {
-        g.grp_start[k] = grp_off[k - 1];
-        g.grp_cta[k - 1] = ctas;
-        ctas += (grp_off[k] - grp_off[k - 1] + G - 1) / G;
+        q.grp_start[k] = grp_off[k - 1];
+        q.grp_cta[k - 1] = c3;
+        c3 += (grp_off[k] - grp_off[k - 1] + kS3Slots / k - 1) / (kS3Slots / k) * q.nsl;
       }
-      g.grp_cta[1] = (grp_off[1] - grp_off[0] + G - 1) / G;
-      g.grp_cta[2] = g.grp_cta[1] + (grp_off[2] - grp_off[1] + G - 1) / G;
-      g.grp_cta[3] = ctas;
-      if (ctas > 0 && use_seg) {
-        SegArgs q{};
-        q.C = int(C);
-        q.L = L;
-        q.nphi = nphi;
-        q.nblk = R / 4;
-        q.G = G;
-        // segments: enough warps to cover the device, P*S <= 512 threads
-        const long long pair_warps = (ctas * P + 31) / 32;
-        const long long want = (148LL * 24 + pair_warps - 1) / std::max(1LL, pair_warps);
-        int S2 = 1;
-        while (S2 * 2 <= want && P * S2 * 2 <= 512 && S2 < 16) S2 *= 2;
-        S2 = std::min(S2, std::max(1, (q.nblk + 1) / 2));
-        q.S = S2;
-        q.cand = d_cand.p;
-        q.cand_idx = d_cidx.p;
-        q.tab = d_tab.p;
-        q.mask = d_mask.p;
-        q.prow_off = d_prow_off.p;
-        q.Z = d_Z.p;
-        q.bv = d_bv.p;
-        q.iagg = d_iagg.p;
-        q.out_maxerr = d_pmaxerr.p;
-        q.out_cand = d_pcand.p;
-        q.e_bar = cfg.e_bar;
-        for (int k = 0; k < 4; ++k) {
-          q.grp_start[k] = g.grp_start[k];
-          q.grp_cta[k] = g.grp_cta[k];
-        }
-        const int Kr = 4 * S2;
-        const size_t buf_e = (size_t(Kr) * 4 + 15) / 16 + size_t(Kr) * L * 2 + size_t(G) * 3 * 2 * Kr;
-        const size_t smem = 2 * buf_e * 16 + 2 * size_t(Kr) * P * 8 + ((size_t(G) * 3 * 2 + 3) & ~size_t(3)) * 4 +
-                            size_t(std::max(S2, 2)) * P * 8 + 64;
-        score_seg_kernel<<<ctas, P * S2, smem, stream>>>(q);
-      } else if (ctas > 0 && use_score3) {
-        S3Args q = s3_args();
-        q.C = int(C);
-        q.R = R;
-        int c3 = 0;
-        for (int k = 1; k <= 3; ++k) {
-          q.grp_start[k] = grp_off[k - 1];
-          q.grp_cta[k - 1] = c3;
-          const int cpc = kS3Slots / k;
-          c3 += (grp_off[k] - grp_off[k - 1] + cpc - 1) / cpc * q.nsl;
-        }
-        q.grp_cta[1] = (grp_off[1] - grp_off[0] + kS3Slots - 1) / kS3Slots * q.nsl;
-        q.grp_cta[2] = q.grp_cta[1] + (grp_off[2] - grp_off[1] + kS3Slots / 2 - 1) / (kS3Slots / 2) * q.nsl;
-        q.grp_cta[3] = c3;
-        if (c3 > 0)
-          score3_kernel<<<c3, s3_threads(), S3Layout{s3_ls(), kS3Slots}.smem_bytes(), stream>>>(q);
-      } else if (ctas > 0 && use_score2) {
-        const size_t smem = Score2Layout{L, G, 3}.smem_bytes(P);
-        score2_kernel<<<ctas, P, smem, stream>>>(g);
-      } else if (ctas > 0 && use_tiles) {
-        constexpr int K = 32;
-        const size_t per_buf = (K * 4 + 15) / 16 + size_t(K) * L * 2 + size_t(G) * 3 * 2 * K;  // double2 units
-        const size_t smem = std::max(2 * per_buf * sizeof(double2) + size_t(G) * 3 * 2 * sizeof(int) + 64,
-                                     2 * size_t(P) * sizeof(double));
-        score_tiles_kernel<<<ctas, P, smem, stream>>>(g);
-      } else if (ctas > 0) {
-        const size_t smem = (2 * size_t(S) * 4 + 3) * size_t(P) * sizeof(double);
-        score_rows_kernel<<<ctas, P * S, smem, stream>>>(g);
+      q.grp_cta[3] = c3;
+      if (c3 > 0) {
+        score3_kernel<<<c3, s3_threads(), S3Layout{s3_ls(), kS3Slots}.smem_bytes(), stream>>>(q);
         launched();
         CK(cudaGetLastError());
       }
@@ -1314,7 +1221,7 @@ struct Engine::Impl {
     launch_score(C);
     const bool naive = !cfg.use_delta;
     argmin_kernel<<<1, 1024, 0, stream>>>(int(std::max(C, 0LL)), L,
-                                          (naive || (cfg.objective == Objective::magnitude && use_score3)) ? s3_ldc() : 0,
+                                          (naive || cfg.objective == Objective::magnitude) ? s3_ldc() : 0,
                                           cfg.e_bar, c0, d_psmice.p, d_pmaxerr.p,
                                           (cfg.objective == Objective::magnitude && !naive) ? d_pcand.p : nullptr,
                                           d_best.p);
@@ -1367,8 +1274,8 @@ struct Engine::Impl {
   size_t enum_smem() const { return pow2_at_least(std::max<size_t>(2 * prob.net.branches.size(), 1)) * sizeof(unsigned); }
 
   bool device_loop_ok(const ReductionConfig& c) const {
-    return !force_host_loop && c.use_delta && c.objective == Objective::magnitude && world == 1 && !profile && use_tiles &&
-           !use_seg && full.bW > 0 && n <= 65535 && enum_smem() + 24 * 1024 <= size_t(optin_smem);
+    return !force_host_loop && c.use_delta && c.objective == Objective::magnitude && world == 1 && !profile &&
+           full.bW > 0 && n <= 65535 && enum_smem() + 24 * 1024 <= size_t(optin_smem);
   }
 
   LoopArgs loop_args() {
@@ -1379,17 +1286,11 @@ struct Engine::Impl {
     a.slack = prob.slack;
     a.L = L;
     a.nphi = nphi;
-    const int P = score_cta_threads();
-    a.G = (P % L == 0) ? P / L : 1;
     a.cap = n;
     a.e_bar = cfg.e_bar;
-    a.nsl = 1;
-    for (int k = 1; k <= 3; ++k) a.cpc[k] = a.G;
-    if (use_score3) {
-      a.nsl = s3_nsl();
-      for (int k = 1; k <= 3; ++k) a.cpc[k] = kS3Slots / k;
-      a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
-    }
+    a.nsl = s3_nsl();
+    for (int k = 1; k <= 3; ++k) a.cpc[k] = kS3Slots / k;
+    a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
     a.has_target = cfg.target_reduction ? 1 : 0;
     a.target = cfg.target_reduction ? *cfg.target_reduction : 0.0;
     a.br_from = d_brf.p;
@@ -1471,32 +1372,6 @@ struct Engine::Impl {
       CK(cudaMemsetAsync(d_tdbg.p, 0, sizeof(unsigned long long) * size_t(n + 1) * 8, stream));
       la.tdbg = d_tdbg.p;
     }
-    // scorer launch (grid sized for the largest candidate set)
-    RowArgs g{};
-    g.L = L;
-    g.nphi = nphi;
-    g.tab = d_tab.p;
-    g.mask = d_mask.p;
-    g.prow_off = d_prow_off.p;
-    g.Z = d_Z.p;
-    g.bv = d_bv.p;
-    g.iagg = d_iagg.p;
-    g.out_smice = d_psmice.p;
-    g.out_maxerr = d_pmaxerr.p;
-    g.G = la.G;
-    g.S = 1;
-    g.cand = d_cand.p;
-    g.cand_idx = d_cidx.p;
-    g.out_cand = d_pcand.p;
-    g.e_bar = cfg.e_bar;
-    g.st = d_loopst.p;
-    g.tdbg = la.tdbg;
-    const int P = score_cta_threads();
-    constexpr int K = 32;
-    const size_t per_buf = (K * 4 + 15) / 16 + size_t(K) * L * 2 + size_t(la.G) * 3 * 2 * K;
-    const size_t score_smem = std::max(2 * per_buf * sizeof(double2) + size_t(la.G) * 3 * 2 * sizeof(int) + 64,
-                                       2 * size_t(P) * sizeof(double));
-    const int score_grid = (2 * nb + la.G - 1) / la.G + 3;
     BaseArgs bb = full.bprog;
     bb.L = L;
     bb.W = full.bW;
@@ -1540,23 +1415,19 @@ struct Engine::Impl {
       // kLoopUnroll iterations per body execution: the conditional relaunch
       // costs a few microseconds, and iterations after the last one are
       // early-exit no-ops (every kernel checks st->done)
+      // score3 grid: persistent over work items, sized for the largest candidate set
+      S3Args q = s3_args();
+      q.st = d_loopst.p;
+      q.tdbg = la.tdbg;
+      int occ = 0;
+      const size_t sm3 = S3Layout{s3_ls(), kS3Slots}.smem_bytes();
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score3_kernel, s3_threads(), sm3));
+      int sms = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      const int items_max = ((2 * nb + 4) / 5 + 3) * s3_nsl();
+      const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
       for (int u = 0; u < kLoopUnroll; ++u) {
-      if (use_score3) {
-        S3Args q = s3_args();
-        q.st = d_loopst.p;
-        q.tdbg = la.tdbg;
-        int occ = 0;
-        const size_t sm3 = S3Layout{s3_ls(), kS3Slots}.smem_bytes();
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score3_kernel, s3_threads(), sm3));
-        int sms = 0;
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-        const int items_max = ((2 * nb + 4) / 5 + 3) * s3_nsl();
-        const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
-        score3_kernel<<<grid3, s3_threads(), sm3, stream>>>(q);
-      } else if (use_score2)
-        score2_kernel<<<score_grid, P, Score2Layout{L, la.G, 3}.smem_bytes(P), stream>>>(g);
-      else
-        score_tiles_kernel<<<score_grid, P, score_smem, stream>>>(g);
+      score3_kernel<<<grid3, s3_threads(), sm3, stream>>>(q);
       pick_commit_kernel<<<1, kLoopThreads, 0, stream>>>(lb);
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
@@ -1853,25 +1724,16 @@ void Engine::loop_score_all(double* smice, std::uint8_t* feasible, double* max_e
   I.upload_iteration(0, C);
   I.launch_score(C);
   // score3 writes scenario-major [L][ldc]; the complex scorer candidate-major [C][L]
-  const bool tr = !I.cfg.use_delta || (I.cfg.objective == Objective::magnitude && I.use_score3);
+  const bool tr = !I.cfg.use_delta || I.cfg.objective == Objective::magnitude;
   const size_t ldc = size_t(I.s3_ldc());
   const size_t npair = tr ? ldc * I.L : size_t(C) * I.L;
-  std::vector<double> ps(npair), pm(npair), pc(static_cast<size_t>(C));
-  const bool mag = I.cfg.use_delta && I.cfg.objective == Objective::magnitude && !I.use_score3;
+  std::vector<double> ps(npair), pm(npair);
   if (C > 0) {
-    if (mag)
-      CK(cudaMemcpyAsync(pc.data(), I.d_pcand.p, pc.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
-    else
-      CK(cudaMemcpyAsync(ps.data(), I.d_psmice.p, ps.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
+    CK(cudaMemcpyAsync(ps.data(), I.d_psmice.p, ps.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
     CK(cudaMemcpyAsync(pm.data(), I.d_pmaxerr.p, pm.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
   }
   CK(cudaStreamSynchronize(I.stream));
-  for (long long c = 0; c < C && mag; ++c) {
-    feasible[c] = pc[size_t(c)] < 0.0 ? 0 : 1;
-    smice[c] = pc[size_t(c)] < 0.0 ? std::numeric_limits<double>::infinity() : pc[size_t(c)];
-    for (int l = 0; l < I.L && max_err; ++l) max_err[size_t(c) * I.L + l] = pm[size_t(c) * I.L + l];
-  }
-  for (long long c = 0; c < C && !mag; ++c) {
+  for (long long c = 0; c < C; ++c) {
     bool feas = true;
     double sum = 0;
     for (int l = 0; l < I.L; ++l) {

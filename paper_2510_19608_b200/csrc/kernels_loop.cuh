@@ -29,7 +29,7 @@ namespace {
 
 struct LoopArgs {
   LoopState* st;
-  int n, nb, slack, L, nphi, G, cap;
+  int n, nb, slack, L, nphi, cap;
   int cpc[4];          // candidates per scorer CTA for each |phi(r)| group (1..3)
   int nsl;             // scenario slices per candidate group (score3), 1 otherwise
   const double* psm;   // score3 per-pair SMICE [L][ldc] (null: pcand holds per-candidate sums)
