@@ -19,6 +19,8 @@ import numpy as np
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "_lib" / "libkronred_b200.so"
+if os.environ.get("KRONRED_LIB"):  # an alternative build of the same library (tools/ variant sweeps)
+    LIB_PATH = Path(os.environ["KRONRED_LIB"])
 
 KRG_OK, KRG_E_VALIDATION, KRG_E_SOLVER, KRG_E_CUDA, KRG_E_INTERNAL = 0, 2, 3, 4, 5
 OBJ_MAGNITUDE, OBJ_COMPLEX = 0, 1

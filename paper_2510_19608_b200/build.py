@@ -65,5 +65,28 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_variant(out_dir: Path, defines: list[str]) -> Path:
+    """Tuning aid: the library with the CUDA engine recompiled under extra
+    -D defines, into out_dir (host objects reused from the main build).
+    Load it with KRONRED_LIB=<out_dir>/libkronred_b200.so."""
+    build()
+    out_dir.mkdir(parents=True, exist_ok=True)
+    objs = []
+    for src in sources():
+        if src.suffix == ".cu":
+            obj = out_dir / (src.name + ".o")
+            _run([NVCC, *NVFLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)])
+        else:
+            obj = OUT / (src.name + ".o")
+        objs.append(obj)
+    lib = out_dir / LIB.name
+    _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    return lib
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    if "--variant" in sys.argv:  # build.py --variant DIR [DEFINE ...]
+        i = sys.argv.index("--variant")
+        print(build_variant(Path(sys.argv[i + 1]), sys.argv[i + 2:]))
+    else:
+        build(force="--force" in sys.argv, verbose=True)

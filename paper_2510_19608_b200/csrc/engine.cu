@@ -1475,6 +1475,12 @@ struct Engine::Impl {
     if (loop_trace && it > 2) {
       std::vector<unsigned long long> T(size_t(n + 1) * 8);
       CK(cudaMemcpy(T.data(), d_tdbg.p, sizeof(unsigned long long) * T.size(), cudaMemcpyDeviceToHost));
+      if (const char* dump = std::getenv("KRONRED_LOOP_TRACE_DUMP")) {  // raw stamps [n+1][8] for tools/
+        if (FILE* f = std::fopen(dump, "wb")) {
+          std::fwrite(T.data(), sizeof(unsigned long long), size_t(it + 1) * 8, f);
+          std::fclose(f);
+        }
+      }
       // per iteration i: score start [i][6], pick [i][0..1], enum for i+1 [i+1][2..3], refresh [i+1][4..5]
       double a_sc = 0, a_pick = 0, a_p2e = 0, a_enum = 0, a_p2r = 0, a_r2s = 0, a_e2s = 0, a_ref = 0, a_tab = 0;
       int cnt = 0;

@@ -67,6 +67,43 @@ struct S3Layout {
   __host__ __device__ size_t smem_bytes() const { return 3 * buf_e() * sizeof(double2) + size_t(G) * 2 * sizeof(int) + 64; }
 };
 
+#ifndef S3_NNMAX
+#define S3_NNMAX 1
+#endif
+#ifndef S3_HH_UNROLL
+#define S3_HH_UNROLL 0
+#endif
+
+// max(a, b) for the scorer's error terms. Every call has at least one operand
+// >= +0 (em = max(m - lo, hi - m) with lo <= hi: if m < lo then hi - m > 0;
+// the running maxima start at +0), and a non-negative double orders like its
+// bit pattern read as a signed 64-bit integer while any negative one (sign bit
+// set) reads as a negative integer. So the integer maximum is the exact
+// floating-point maximum here, and it runs on the integer pipes instead of
+// a DSETP on the FP64 pipe.
+__device__ __forceinline__ double s3max(double a, double b) {
+#if S3_NNMAX
+  const long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  return __longlong_as_double(x > y ? x : y);
+#else
+  return dmax(a, b);
+#endif
+}
+
+// max_err over a pass: a pairwise tree (max is exact and order-free), so the
+// dependent chain is log2(NR) deep instead of NR
+template <int NR>
+__device__ __forceinline__ double s3_tree_max(const double (&em)[NR]) {
+  double t[NR];
+#pragma unroll
+  for (int v = 0; v < NR; ++v) t[v] = em[v];
+#pragma unroll
+  for (int w = NR / 2; w >= 1; w /= 2)
+#pragma unroll
+    for (int v = 0; v < w; ++v) t[v] = s3max(t[v], t[v + w]);
+  return t[0];
+}
+
 // NR plain rows: Vc, |Vc|, exact cluster error, then NR super-node
 // boundaries of the ordered fold (ILP NR until the fold).
 template <int NL, int NR>
@@ -87,7 +124,7 @@ __device__ __forceinline__ void s3_plain(const double2* __restrict__ bvp, const 
     const double s2 = dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy));
     bad = bad || !sqrt_fast_ok(s2);
     const double m = sqrt_rn_fast(s2);
-    em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
+    em[v] = s3max(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
   }
   if (__any_sync(0xffffffffu, bad)) {
 #pragma unroll
@@ -101,15 +138,15 @@ __device__ __forceinline__ void s3_plain(const double2* __restrict__ bvp, const 
         vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
       }
       const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
-      em[v] = dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
+      em[v] = s3max(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
     }
   }
 #pragma unroll
   for (int v = 0; v < NR; ++v) {
     smice = dev::dadd(smice, cm);
     cm = em[v];
-    mx = dmax(mx, em[v]);
   }
+  mx = s3max(mx, s3_tree_max(em));
 }
 
 __device__ __forceinline__ bool s3_block_plain(uint4 e4) {
@@ -171,7 +208,7 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
     if (t >= f.ts0 && t < f.ts1 && ph != 3u) {
       const double rl = ph == 0u ? f.rlo0 : (ph == 1u ? f.rlo1 : f.rlo2);
       const double rh = ph == 0u ? f.rhi0 : (ph == 1u ? f.rhi1 : f.rhi2);
-      e = dmax(e, dmax(dev::dsub(m, rl), dev::dsub(rh, m)));
+      e = s3max(e, s3max(dev::dsub(m, rl), dev::dsub(rh, m)));
     }
     return ((t >= f.tr0 && t < f.tr1) || ph == 3u) ? 0.0 : e;
   };
@@ -188,7 +225,7 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
     const double s2 = dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy));
     bad = bad || !sqrt_fast_ok(s2);
     const double m = sqrt_rn_fast(s2);
-    em[v] = fix(v, m, dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m)));
+    em[v] = fix(v, m, s3max(dev::dsub(m, b1.x), dev::dsub(b1.y, m)));
   }
   if (__any_sync(0xffffffffu, bad)) {
 #pragma unroll
@@ -202,7 +239,7 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
         vy = dev::dadd(vy, dev::dadd(dev::dmul(cv[k].x, dz.y), dev::dmul(cv[k].y, dz.x)));
       }
       const double m = dev::dsqrt(dev::dadd(dev::dmul(vx, vx), dev::dmul(vy, vy)));
-      em[v] = fix(v, m, dmax(dev::dsub(m, b1.x), dev::dsub(b1.y, m)));
+      em[v] = fix(v, m, s3max(dev::dsub(m, b1.x), dev::dsub(b1.y, m)));
     }
   }
 #pragma unroll
@@ -211,9 +248,9 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
       smice = dev::dadd(smice, cm);
       cm = 0.0;
     }
-    cm = dmax(cm, em[v]);
-    mx = dmax(mx, em[v]);
+    cm = s3max(cm, em[v]);
   }
+  mx = s3max(mx, s3_tree_max(em));
 }
 
 template <int NL, int LSC>  // LSC: compile-time slice width (0: runtime a.Ls)
@@ -280,6 +317,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   const int bv_dst = (bv_ch & 1) * Ls + (bv_ch >> 1);  // shared row layout [base x Ls][bounds x Ls]
   const size_t bv_off = size_t(sl) * Ls * 2;
 
+  const int nz = Gk * NL * 2 * K3;  // Z staging slots per tile (16-byte)
   auto stage = [&](int j, int b) {
     const int t0 = j * K3;
     for (int i = tid; i < K3 / 4; i += P) cp_async16(tab_s(b) + 4 * i, a.tab + t0 + 4 * i);
@@ -297,7 +335,6 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
         cp_async16(bv_s(b) + size_t(u) * RS + (ch & 1) * Ls + (ch >> 1), a.bv + rho * 2 * L + bv_off + ch);
       }
     }
-    const int nz = Gk * NL * 2 * K3;
     for (int i = tid; i < nz; i += P) {
       const int u = i % K3;
       const int col = zcol[i / K3];
@@ -305,27 +342,40 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
       cp_async16(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(col) * nphi + rho);
     }
   };
-  // Fast staging: each thread owns at most two bv rows and one Z row of every
-  // tile, so the table entries it needs are prefetched into registers one
-  // tile ahead (no dependent global load in front of each cp.async).
-  const bool fst = bv_fixed && (P % K3) == 0 && 2 * bv_du >= K3;
+  // Fast staging: each thread owns at most two bv rows and one table row of
+  // the Z block in every tile, and at most four fixed Z slots (same column for
+  // the whole item), so the column sources are resolved once and the table
+  // entries are prefetched raw one tile ahead: no dependent load in front of a
+  // cp.async, and the prefetch is not consumed until the next tile.
+  const bool fst = bv_fixed && (P % K3) == 0 && 2 * bv_du >= K3 && nz <= 4 * P;
   const int u_a = bv_u0, u_b = bv_u0 + bv_du, u_z = tid % K3;
-  auto load_rho = [&](int j, unsigned (&rr)[3]) {
+  const double2* zsrc[4];
+  int zdst[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = min(tid + q * P, nz - 1);
+    zsrc[q] = a.Z + size_t(zcol[i / K3]) * nphi;
+    zdst[q] = i + i / (NL * 2 * K3);
+  }
+  auto load_rho = [&](int j, unsigned (&rr)[3]) {  // raw table entries: (rho << 3) | flags
     const int t0 = j * K3;
-    rr[0] = (j < ntiles && u_a < K3) ? __ldg(a.tab + t0 + u_a) >> 3 : 0u;
-    rr[1] = (j < ntiles && u_b < K3) ? __ldg(a.tab + t0 + u_b) >> 3 : 0u;
-    rr[2] = j < ntiles ? __ldg(a.tab + t0 + u_z) >> 3 : 0u;
+    rr[0] = (j < ntiles && u_a < K3) ? __ldg(a.tab + t0 + u_a) : 0u;
+    rr[1] = (j < ntiles && u_b < K3) ? __ldg(a.tab + t0 + u_b) : 0u;
+    rr[2] = j < ntiles ? __ldg(a.tab + t0 + u_z) : 0u;
   };
   auto stage_fast = [&](int j, int b, const unsigned (&rr)[3]) {
     const int t0 = j * K3;
     if (tid < K3 / 4) cp_async16(tab_s(b) + 4 * tid, a.tab + t0 + 4 * tid);
     if (bv_ch < 2 * nsc) {
-      if (u_a < K3) cp_async16(bv_s(b) + size_t(u_a) * RS + bv_dst, a.bv + size_t(rr[0]) * 2 * L + bv_off + bv_ch);
-      if (u_b < K3) cp_async16(bv_s(b) + size_t(u_b) * RS + bv_dst, a.bv + size_t(rr[1]) * 2 * L + bv_off + bv_ch);
+      if (u_a < K3)
+        cp_async16(bv_s(b) + size_t(u_a) * RS + bv_dst, a.bv + size_t(rr[0] >> 3) * 2 * L + bv_off + bv_ch);
+      if (u_b < K3)
+        cp_async16(bv_s(b) + size_t(u_b) * RS + bv_dst, a.bv + size_t(rr[1] >> 3) * 2 * L + bv_off + bv_ch);
     }
-    const int nz = Gk * NL * 2 * K3;
-    for (int i = tid; i < nz; i += P)
-      cp_async16(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(zcol[i / K3]) * nphi + rr[2]);
+    const size_t rz = rr[2] >> 3;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (tid + q * P < nz) cp_async16(z_s(b) + zdst[q], zsrc[q] + rz);
   };
   auto form_d = [&](int b) {  // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row)
     double2* zz = z_s(b);
@@ -341,6 +391,9 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
 
   double smice = 0.0, mx = 0.0, cm = 0.0;
   unsigned rn[3];
+#ifdef S3_TIMING  // tuning aid: per-phase cycle counts of CTA 0's warps
+  long long tm_pro = clock64(), tm_wait = 0, tm_stage = 0, tm_rho = 0, tm_fd = 0, tm_comp = 0, tm_x;
+#endif
   if (fst) {
     unsigned r0[3], r1[3];
     load_rho(0, r0);
@@ -359,22 +412,48 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   cp_async_wait1();
   __syncthreads();
   form_d(0);
-  bool tflag_next = a.tplain[0] != 0;
+#ifdef S3_TIMING
+  tm_pro = clock64() - tm_pro;
+#endif
+  unsigned tflag_next = a.tplain[0];  // raw byte: tested one tile later
   for (int j = 0; j < ntiles; ++j) {
     const int b = j % 3;
-    const bool tflag = tflag_next;
-    if (j + 1 < ntiles) tflag_next = a.tplain[j + 1] != 0;
+    const bool tflag = tflag_next != 0u;
+    if (j + 1 < ntiles) tflag_next = a.tplain[j + 1];
+#ifdef S3_TIMING
+    tm_x = clock64();
+#endif
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
+#ifdef S3_TIMING
+    tm_wait += clock64() - tm_x;
+    tm_x = clock64();
+#endif
     if (fst) {
       if (j + 2 < ntiles) stage_fast(j + 2, (j + 2) % 3, rn);
       cp_async_commit();
+#ifdef S3_TIMING
+      tm_stage += clock64() - tm_x;
+      tm_x = clock64();
+#endif
       load_rho(j + 3, rn);  // consumed next iteration: latency hidden by this tile's compute
+#ifdef S3_TIMING
+      tm_rho += clock64() - tm_x;
+      tm_x = clock64();
+#endif
     } else {
       if (j + 2 < ntiles) stage(j + 2, (j + 2) % 3);
       cp_async_commit();
     }
+#ifdef S3_TIMING
+    tm_stage += clock64() - tm_x;
+    tm_x = clock64();
+#endif
     if (j + 1 < ntiles) form_d((j + 1) % 3);
+#ifdef S3_TIMING
+    tm_fd += clock64() - tm_x;
+    tm_x = clock64();
+#endif
     const int t0 = j * K3;
     const unsigned* tb = tab_s(b);
     const double2* bvp = bv_s(b) + size_t(ll);  // this thread's scenario: base at +0, bounds at +Ls per row
@@ -385,15 +464,27 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     // flag-driven fold
     constexpr int NRT = NL == 1 ? 8 : 4;  // rows per pass (register budget)
     if (tflag && !__any_sync(0xffffffffu, j == (ts0 >> 4) || j == (tr0 >> 4))) {
+#if S3_HH_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
       for (int hh = 0; hh < K3 / NRT; ++hh) s3_plain<NL, NRT>(bvp, zp, RS, NRT * hh, cv, smice, cm, mx);
     } else {
 #pragma unroll 1
       for (int hh = 0; hh < K3 / NRT; ++hh)
         s3_rows_gen<NL, NRT>(bvp, zp, RS, NRT * hh, t0, tb, cv, fx, smice, cm, mx);
     }
+#ifdef S3_TIMING
+    tm_comp += clock64() - tm_x;
+#endif
   }
   smice = dev::dadd(smice, cm);
+#ifdef S3_TIMING
+  if (blockIdx.x == 0 && (tid & 31) == 0 && a.st && (a.st->iter == 1 || a.st->iter == 100 || a.st->iter == 850))
+    printf("s3 timing iter %d warp %d NL %d tiles %d: prologue %lld wait+sync %lld stage %lld rho %lld form_d %lld compute %lld\n",
+           a.st->iter, tid >> 5, NL, ntiles, tm_pro, tm_wait, tm_stage, tm_rho, tm_fd, tm_comp);
+#endif
   if (valid) {
     const size_t o = size_t(l) * a.ldc + a.cand_idx[c];
     a.out_sm[o] = smice;
