@@ -602,6 +602,8 @@ struct Engine::Impl {
             }
         }
       }
+      if (const char* e = std::getenv("KRONRED_REFRESH_W"))  // tuning aid: cap scenario warps per CTA
+        d.bW = std::max(1, std::min(d.bW, std::atoi(e)));
       d.bsmem = int(fx + size_t(std::max(d.bW, 1)) * per_warp);
     }
     d.meta.alloc(meta.size());
@@ -1368,8 +1370,8 @@ struct Engine::Impl {
     }
     LoopArgs la = loop_args();
     if (loop_trace) {
-      d_tdbg.alloc(size_t(n + 1) * 8);
-      CK(cudaMemsetAsync(d_tdbg.p, 0, sizeof(unsigned long long) * size_t(n + 1) * 8, stream));
+      d_tdbg.alloc(size_t(n + 1) * kTdbg);
+      CK(cudaMemsetAsync(d_tdbg.p, 0, sizeof(unsigned long long) * size_t(n + 1) * kTdbg, stream));
       la.tdbg = d_tdbg.p;
     }
     BaseArgs bb = full.bprog;
@@ -1473,11 +1475,11 @@ struct Engine::Impl {
     launches += 4LL * ((st.iter + kLoopUnroll) / kLoopUnroll * kLoopUnroll);
     const int it = st.iter;
     if (loop_trace && it > 2) {
-      std::vector<unsigned long long> T(size_t(n + 1) * 8);
+      std::vector<unsigned long long> T(size_t(n + 1) * kTdbg);
       CK(cudaMemcpy(T.data(), d_tdbg.p, sizeof(unsigned long long) * T.size(), cudaMemcpyDeviceToHost));
       if (const char* dump = std::getenv("KRONRED_LOOP_TRACE_DUMP")) {  // raw stamps [n+1][8] for tools/
         if (FILE* f = std::fopen(dump, "wb")) {
-          std::fwrite(T.data(), sizeof(unsigned long long), size_t(it + 1) * 8, f);
+          std::fwrite(T.data(), sizeof(unsigned long long), size_t(it + 1) * kTdbg, f);
           std::fclose(f);
         }
       }
@@ -1485,8 +1487,8 @@ struct Engine::Impl {
       double a_sc = 0, a_pick = 0, a_p2e = 0, a_enum = 0, a_p2r = 0, a_r2s = 0, a_e2s = 0, a_ref = 0, a_tab = 0;
       int cnt = 0;
       for (int i = 1; i + 1 < it; ++i) {
-        const unsigned long long* c = &T[size_t(i) * 8];
-        const unsigned long long* nx = &T[size_t(i + 1) * 8];
+        const unsigned long long* c = &T[size_t(i) * kTdbg];
+        const unsigned long long* nx = &T[size_t(i + 1) * kTdbg];
         a_sc += double(c[0] - c[6]);
         a_pick += double(c[1] - c[0]);
         a_p2e += double(nx[2] - c[1]);

@@ -24,6 +24,17 @@ enum CMode { CM_FULL = 0, CM_BASE = 1, CM_ZCOL = 2 };
 // Device-resident loop state (kernels_loop.cuh): the iteration's sizes and
 // scorer grid layout, written by the enumeration kernel, read by the scorer,
 // the pick/commit kernel and the base refresh (which all exit when done).
+// loop timeline stamps per iteration (KRONRED_LOOP_TRACE): 0/1 pick start/end,
+// 2/3 enum start/end, 4/5 refresh start/end (CTA 0), 6 score start, 7 enum
+// table done, 8 refresh staged (CTA 0), 9 refresh walk done (CTA 0), 10 last
+// refresh CTA end
+constexpr int kTdbg = 16;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct LoopState {
   int done, iter, ns, C, R, err;
   int last_s, last_r;  // the last committed candidate (incremental base refresh)
@@ -530,14 +541,66 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   const int4* bs = reinterpret_cast<const int4*>(M + a.bslot);
   const int4* bx = reinterpret_cast<const int4*>(M + a.bext);
   const int2* be = reinterpret_cast<const int2*>(M + a.bent);
-  int4 rc = bs[lane];
-  int4 rx = bx[lane];
-  for (int br = 0; br < a.nbr; ++br) {
-    const int4 nx = bs[(br + 1) * 32 + lane];
-    const int4 nxx = bx[(br + 1) * 32 + lane];
-    if (rc.x >= 0 && rx.x == 0) {
-      const C2 xj = lds2(xs + rc.z), aa = cfl<SM>(cs, cf, rc.w), pv = cfl<SM>(cs, cf, rc.y), t = lds2(xs + rc.x);
-      C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj)));
+  const int nbr = a.nbr;
+  // Opaque copies: keeps the shared-window bases in registers instead of
+  // re-deriving them (S2R) in front of the loads of every round.
+  asm volatile("mov.b32 %0, %0;" : "+r"(xs));
+  asm volatile("mov.b32 %0, %0;" : "+r"(cs));
+  // Records are read two rounds ahead (the arrays carry one padding round, so
+  // the index is clamped to it); a scalar step's coefficients and its own
+  // forward value t_k one round ahead (the factor is read-only during the
+  // sweep and x_k is written only by its own step).
+  const int4* bsl = bs + lane;
+  const int4* bxl = bx + lane;
+  asm volatile("mov.b64 %0, %0;" : "+l"(bsl));
+  asm volatile("mov.b64 %0, %0;" : "+l"(bxl));
+  int4 rc = bsl[0], rx = bxl[0];
+  int4 nx = bsl[min(1, nbr) * 32], nxx = bxl[min(1, nbr) * 32];
+  const bool sc0 = rc.x >= 0 && rx.x == 0;
+  C2 aa = sc0 ? cfl<SM>(cs, cf, rc.w) : C2{0.0, 0.0}, pv = sc0 ? cfl<SM>(cs, cf, rc.y) : C2{0.0, 0.0};
+  C2 t = sc0 ? lds2(xs + rc.x) : C2{0.0, 0.0};
+#ifdef BR_TRACE  // tuning aid: per-round cycles of CTA 0 / warp 0 (debug refresh only)
+  long long tr_t[80], tr_b[80], tr_c[80];
+  unsigned tr_a[80], tr_g[80];
+  for (int i = 0; i < 80; ++i) tr_b[i] = tr_c[i] = 0;
+  const bool tr_on = a.dbg && blockIdx.x == 0 && threadIdx.x < 32;
+#endif
+  for (int br = 0; br < nbr; ++br) {
+#ifdef BR_TRACE
+    if (tr_on && br < 80) {
+      tr_g[br] = __ballot_sync(0xffffffffu, rc.x >= 0 && rx.x != 0);
+      tr_a[br] = __ballot_sync(0xffffffffu, rc.x >= 0);
+      tr_t[br] = clock64();
+    }
+#endif
+    // the parent's value first: it is the round's critical load (the shared
+    // loads are ordered volatile asm, so it is issued ahead of the rest)
+    const C2 xj = lds2(xs + (rc.x >= 0 ? rc.z : 0));
+    // next round's scalar operands right behind it, so the shared-memory
+    // pipe drains them while this round's products run (x_n is written only in
+    // its own round, the factor not at all)
+    const bool scn = nx.x >= 0 && nxx.x == 0;
+    const C2 aa_n = cfl<SM>(cs, cf, scn ? nx.w : 0), pv_n = cfl<SM>(cs, cf, scn ? nx.y : 0);
+    const C2 t_n = lds2(xs + (scn ? nx.x : 0));
+    const int4 nx2 = bsl[min(br + 2, nbr) * 32], nxx2 = bxl[min(br + 2, nbr) * 32];
+    const bool sc = rc.x >= 0 && rx.x == 0;
+    if (__all_sync(0xffffffffu, rc.x < 0 || (rx.x == 0 && rx.w == 0))) {
+      // every step of the round is scalar with the single coupling to its
+      // parent: x_k = t_k - (0 + pinv (0 + (0 + A x_p))) (Mat3c * Vec3c from
+      // zero, coupling sum from zero; adding +0 twice equals adding it once)
+      if (rc.x >= 0) {
+#ifdef BR_TRACE
+        if (tr_on && br < 80 && xj.x != 1.2345e300) tr_b[br] = clock64();
+#endif
+        const C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj));
+        const C2 res = dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc)));
+#ifdef BR_TRACE
+        if (tr_on && br < 80 && res.x != 1.2345e300) tr_c[br] = clock64();
+#endif
+        sts2(xs + rc.x, res);
+      }
+    } else if (sc) {
+      C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj));
       int e = rx.z;
       const int e_end = rx.z + rx.w;
 #pragma unroll 1
@@ -582,10 +645,26 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
         st2(x + xk + r, dev::csub(ld2(x + xk + r), corr));
       }
     }
+    aa = aa_n;
+    pv = pv_n;
+    t = t_n;
     rc = nx;
     rx = nxx;
+    nx = nx2;
+    nxx = nxx2;
+#ifndef BR_NOSYNC
     __syncwarp();
+#endif
   }
+#ifdef BR_TRACE
+  if (tr_on && lane == 0) {
+    const long long tend = clock64();
+    for (int br = 0; br < nbr && br < 80; ++br)
+      printf("round %d: %lld cycles active %d general %d | xj at %lld, result at %lld\n", br,
+             (br + 1 < nbr && br + 1 < 80 ? tr_t[br + 1] : tend) - tr_t[br], __popc(tr_a[br]), __popc(tr_g[br]),
+             tr_b[br] ? tr_b[br] - tr_t[br] : -1LL, tr_c[br] ? tr_c[br] - tr_t[br] : -1LL);
+  }
+#endif
 }
 
 // SM: factor and program staged in shared memory (TMA); otherwise they are
@@ -599,7 +678,7 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    a.tdbg[size_t(a.st->iter) * 8 + 4] = t;
+    a.tdbg[size_t(a.st->iter) * kTdbg + 4] = t;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rhs = blockIdx.x * a.W + warp;
@@ -631,6 +710,7 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   __syncthreads();
   mbar_wait(&bar, 0);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[0] = clock64();
+  if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 8] = globaltimer_ns();
   if (warp >= nw) return;
   double2* x = xall + size_t(warp) * a.nphi;
   for (int k = lane; k < a.nkept; k += 32) {
@@ -655,39 +735,78 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     if (a.tfwd)  // keep the forward values for the next (incremental) refresh
       for (int r = lane; r < a.nphi; r += 32) a.tfwd[size_t(rhs) * a.nphi + r] = x[r];
   } else if (lane == 0) {
-    // walk the ancestors of the two changed nodes in elimination order
+    // Walk the ancestors of the two changed nodes in elimination order. The
+    // two path heads keep their walk entry and step records in registers; a
+    // step issues its parent's record loads before its own arithmetic, and a
+    // scalar step takes its right-hand side straight from the staged copy
+    // (same operations and order as tree_fwd_step).
     const int4* W = reinterpret_cast<const int4*>(M + a.walk);
+    const double2* xr = stage_rhs ? xall + size_t(a.W + warp) * a.nphi : a.iaggp + size_t(rhs) * a.nphi;
+    double2* tf = a.tfwd + size_t(rhs) * a.nphi;
+    const int4 none = make_int4(-1, -1, 0x7fffffff, -1);
     int na = a.st ? a.st->last_s : a.inc_s, nb = a.st ? a.st->last_r : a.inc_r;
-    if (na >= 0 && W[na].x < 0) na = -1;  // kept (slack): no forward step
-    if (nb >= 0 && W[nb].x < 0) nb = -1;
+    int4 wa = na >= 0 ? W[na] : none, wb = nb >= 0 ? W[nb] : none;
+    if (wa.x < 0) na = -1;  // kept (slack): no forward step
+    if (wb.x < 0) nb = -1;
+    int4 ra = na >= 0 ? fs[wa.x] : none, xa = na >= 0 ? fx[wa.x] : none;
+    int4 rb = nb >= 0 ? fs[wb.x] : none, xb = nb >= 0 ? fx[wb.x] : none;
     while (na >= 0 || nb >= 0) {
-      const int sa = na >= 0 ? W[na].z : 0x7fffffff, sb = nb >= 0 ? W[nb].z : 0x7fffffff;
-      const int k = sa <= sb ? na : nb;
-      const int4 wk = W[k];
-      const int4 rc = fs[wk.x], rx = fx[wk.x];
-      // the node's own right-hand side (its aggregated injection), then its step
-      const int xk = rc.x >> 4, mk = rc.z >= 0 ? 1 : rx.y;
-      const double2* xr = stage_rhs ? xall + size_t(a.W + warp) * a.nphi : a.iaggp + size_t(rhs) * a.nphi;
-      for (int i = 0; i < mk; ++i) x[xk + i] = xr[xk + i];
-      asm volatile("" ::: "memory");  // the step reads x through ld.shared asm
-      tree_fwd_step<SM>(rc, rx, xs, cs, x, cf, fe);
-      asm volatile("" ::: "memory");
-      for (int i = 0; i < mk; ++i) a.tfwd[size_t(rhs) * a.nphi + xk + i] = x[xk + i];
-      const int up = wk.y >= 0 && W[wk.y].x >= 0 ? wk.y : -1;  // stop below kept nodes
-      if (sa <= sb) na = up;
-      if (sb <= sa) nb = up;
+      const bool ta = na >= 0 && (nb < 0 || wa.z <= wb.z);
+      const bool tb = nb >= 0 && (na < 0 || wb.z <= wa.z);
+      const int4 wk = ta ? wa : wb, rc = ta ? ra : rb, rx = ta ? xa : xb;
+      const int4 wu = wk.y >= 0 ? W[wk.y] : none;  // the parent's walk entry, in flight during the step
+      const int xk = rc.x >> 4;
+      if (rc.x >= 0 && rc.z >= 0) {
+        const C2 b0 = ld2(xr + xk), tj = lds2(xs + rc.z), t1 = lds2(xs + rx.x);
+        const C2 aa = cfl<SM>(cs, cf, rc.w), pv = cfl<SM>(cs, cf, rc.y), a1 = cfl<SM>(cs, cf, rx.y);
+        const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
+        const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
+        C2 bb = dev::csub(dev::csub(b0, u0), u1);
+        for (int e = rx.z; e < rx.z + rx.w; ++e) {  // further children, elimination order
+          const int2 en = fe[e];
+          bb = dev::csub(bb, dev::cadd(C2{0.0, 0.0},
+                                       dev::cmul(cfl<SM>(cs, cf, en.y * 16), lds2(xs + (en.x & 0xffffff) * 16))));
+        }
+        const C2 v = dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, bb));
+        sts2(xs + rc.x, v);
+        st2(tf + xk, v);
+      } else {
+        // general step: the right-hand side into x, then tree_fwd_step
+        const int mk = rx.y;
+        for (int i = 0; i < mk; ++i) x[xk + i] = xr[xk + i];
+        asm volatile("" ::: "memory");  // the step reads x through ld.shared asm
+        tree_fwd_step<SM>(rc, rx, xs, cs, x, cf, fe);
+        asm volatile("" ::: "memory");
+        for (int i = 0; i < mk; ++i) tf[xk + i] = x[xk + i];
+      }
+      const int up = wk.y >= 0 && wu.x >= 0 ? wk.y : -1;  // stop below kept nodes
+      const int4 ru = up >= 0 ? fs[wu.x] : none, xu = up >= 0 ? fx[wu.x] : none;
+      if (ta) {
+        na = up;
+        wa = wu;
+        ra = ru;
+        xa = xu;
+      }
+      if (tb) {
+        nb = up;
+        wb = wu;
+        rb = ru;
+        xb = xu;
+      }
     }
   }
   __syncwarp();  // the walk (lane 0) wrote x
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
+  if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 9] = globaltimer_ns();
   tree_backward<SM>(a, M, xs, cs, x, cf, lane);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
   for (int r = lane; r < a.nphi; r += 32) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
   if (a.tdbg && blockIdx.x == 0 && tid == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    a.tdbg[size_t(a.st->iter) * 8 + 5] = t;
+    a.tdbg[size_t(a.st->iter) * kTdbg + 5] = t;
   }
+  if (a.tdbg && lane == 0) atomicMax(a.tdbg + size_t(a.st->iter) * kTdbg + 10, globaltimer_ns());
 }
 
 // cfac[i] = (src >= 0 ? (src & 1 ? pinv : blocks)[src >> 1] : 0)

@@ -82,6 +82,53 @@ __device__ __forceinline__ void tab_step(int k, int& q, int& adv) {
   }
 }
 
+// Composition of transducer maps over a chunk of super-nodes: for each start
+// state s (rows mod 4 so far), the end state (2 bits each, packed) and the
+// rows advanced. compose(A, B) = A then B.
+struct TabMap {
+  unsigned q;  // 4 x 2-bit end states
+  int a0, a1, a2, a3;
+};
+__device__ __forceinline__ int tab_sel(const TabMap& m, unsigned s) {
+  return s == 0u ? m.a0 : (s == 1u ? m.a1 : (s == 2u ? m.a2 : m.a3));
+}
+__device__ __forceinline__ TabMap tab_compose(const TabMap& A, const TabMap& B) {
+  TabMap r;
+  r.q = 0u;
+  unsigned q1;
+  q1 = A.q & 3u;
+  r.q |= ((B.q >> (2u * q1)) & 3u);
+  r.a0 = A.a0 + tab_sel(B, q1);
+  q1 = (A.q >> 2) & 3u;
+  r.q |= ((B.q >> (2u * q1)) & 3u) << 2;
+  r.a1 = A.a1 + tab_sel(B, q1);
+  q1 = (A.q >> 4) & 3u;
+  r.q |= ((B.q >> (2u * q1)) & 3u) << 4;
+  r.a2 = A.a2 + tab_sel(B, q1);
+  q1 = (A.q >> 6) & 3u;
+  r.q |= ((B.q >> (2u * q1)) & 3u) << 6;
+  r.a3 = A.a3 + tab_sel(B, q1);
+  return r;
+}
+__device__ __forceinline__ TabMap tab_shfl_up(const TabMap& m, int d) {
+  TabMap r;
+  r.q = __shfl_up_sync(0xffffffffu, m.q, d);
+  r.a0 = __shfl_up_sync(0xffffffffu, m.a0, d);
+  r.a1 = __shfl_up_sync(0xffffffffu, m.a1, d);
+  r.a2 = __shfl_up_sync(0xffffffffu, m.a2, d);
+  r.a3 = __shfl_up_sync(0xffffffffu, m.a3, d);
+  return r;
+}
+// inclusive warp scan of maps (lane order = super-node order)
+__device__ __forceinline__ TabMap tab_warp_scan(TabMap m, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const TabMap p = tab_shfl_up(m, d);
+    if (lane >= d) m = tab_compose(p, m);
+  }
+  return m;
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -91,8 +138,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   extern __shared__ unsigned keys[];  // [pow2 >= 2n]
   __shared__ int s_cnt;
-  __shared__ unsigned char mq[kLoopThreads][4];
-  __shared__ int ma[kLoopThreads][4];
+  __shared__ TabMap wmap[kLoopThreads / 32];
   __shared__ unsigned long long gscan[kLoopThreads / 32];
   LoopState* st = a.st;
   const int tid = threadIdx.x;
@@ -101,44 +147,60 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     return;
   }
   const int ns = st->ns;
-  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * 8 + 2] = globaltimer();
+  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 2] = globaltimer();
+#ifdef ENUM_TIMING
+  long long et[9];
+#endif
 
+#ifdef ENUM_TIMING
+  if (tid == 0) et[0] = clock64();
+#endif
   // ---- row table over the active super-nodes ------------------------------
   const int ch = (ns + kLoopThreads - 1) / kLoopThreads;
   const int b0 = min(ns, tid * ch), b1 = min(ns, b0 + ch);
-  for (int q0 = 0; q0 < 4; ++q0) {
-    int q = q0, adv = 0;
-    for (int k = b0; k < b1; ++k) tab_step(__popc(a.mask[a.sn[k]]), q, adv);
-    mq[tid][q0] = (unsigned char)q;
-    ma[tid][q0] = adv;
-  }
-  __syncthreads();
-  // inclusive Hillis-Steele scan of map composition (earlier map first)
-  for (int d = 1; d < kLoopThreads; d <<= 1) {
-    unsigned char nq[4];
-    int na[4];
-    const bool act = tid >= d;
-    if (act) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int q1 = mq[tid - d][q];
-        nq[q] = mq[tid][q1];
-        na[q] = ma[tid - d][q] + ma[tid][q1];
-      }
-    }
-    __syncthreads();
-    if (act) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        mq[tid][q] = nq[q];
-        ma[tid][q] = na[q];
-      }
-    }
-    __syncthreads();
-  }
+  TabMap tmap;
+  tmap.q = 0u;
   {
-    int q = tid == 0 ? 0 : mq[tid - 1][0];
-    int t = tid == 0 ? 0 : ma[tid - 1][0];
+    int adv4[4];
+#pragma unroll
+    for (int q0 = 0; q0 < 4; ++q0) {
+      int q = q0, adv = 0;
+      for (int k = b0; k < b1; ++k) tab_step(__popc(a.mask[a.sn[k]]), q, adv);
+      tmap.q |= unsigned(q) << (2 * q0);
+      adv4[q0] = adv;
+    }
+    tmap.a0 = adv4[0];
+    tmap.a1 = adv4[1];
+    tmap.a2 = adv4[2];
+    tmap.a3 = adv4[3];
+  }
+  // block scan of map composition (earlier map first): warp shuffles, the
+  // warp totals scanned by warp 0, two barriers
+#ifdef ENUM_TIMING
+  if (tid == 0) et[1] = clock64();
+#endif
+  const int lane = tid & 31, warp = tid >> 5;
+  const TabMap tincl = tab_warp_scan(tmap, lane);
+  if (lane == 31) wmap[warp] = tincl;
+  __syncthreads();
+  if (warp == 0) wmap[lane] = tab_warp_scan(wmap[lane], lane);
+  __syncthreads();
+#ifdef ENUM_TIMING
+  if (tid == 0) et[2] = clock64();
+#endif
+  {
+    // state and table row entering this thread's chunk (from state 0 at row 0)
+    int q = 0, t = 0;
+    if (warp > 0) {
+      const TabMap& w = wmap[warp - 1];
+      q = int(w.q & 3u);
+      t = w.a0;
+    }
+    const TabMap ex = tab_shfl_up(tincl, 1);
+    if (lane > 0) {
+      t += tab_sel(ex, unsigned(q));
+      q = int((ex.q >> (2 * q)) & 3u);
+    }
     for (int k = b0; k < b1; ++k) {
       const int i = a.sn[k];
       const unsigned m = a.mask[i];
@@ -159,15 +221,18 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     }
     if (tid == kLoopThreads - 1) {
       // tail: close the last block and add the scorer's tile padding
-      const int tend = ma[kLoopThreads - 1][0];
+      const int tend = wmap[kLoopThreads / 32 - 1].a0;
       const int R = (tend + 3) & ~3;
       for (int u = tend; u < R + kTabPadRows; ++u) a.tab[u] = kPadEntry;
       st->R = R;
     }
   }
 
+#ifdef ENUM_TIMING
+  if (tid == 0) et[3] = clock64();
+#endif
   // ---- candidates: super-node edges, both directions, filtered ------------
-  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * 8 + 7] = globaltimer();
+  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 7] = globaltimer();
   if (tid == 0) s_cnt = 0;
   __syncthreads();
   // warp-aggregated slot allocation (one shared atomic per warp and direction)
@@ -194,6 +259,9 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     if (e1) keys[base + __popc(m1 & lane_lt)] = k1;
     if (e2) keys[base + n1 + __popc(m2 & lane_lt)] = k2;
   }
+#ifdef ENUM_TIMING
+  if (tid == 0) et[4] = clock64();
+#endif
   __syncthreads();
   const int C = s_cnt;
   if (C == 0) {
@@ -223,11 +291,17 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
       }
       __syncthreads();
     }
+#ifdef ENUM_TIMING
+  if (tid == 0) et[5] = clock64();
+#endif
   for (int i = tid; i < C; i += kLoopThreads) {
     a.cs[i] = int(keys[i] >> 16);
     a.cr[i] = int(keys[i] & 0xffffu);
   }
 
+#ifdef ENUM_TIMING
+  if (tid == 0) et[6] = clock64();
+#endif
   // ---- group by |phi(r)| (stable): packed 3 x 21-bit counters, block scan --
   const int cch = (C + kLoopThreads - 1) / kLoopThreads;
   const int c0 = min(C, tid * cch), c1 = min(C, c0 + cch);
@@ -235,7 +309,6 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   for (int i = c0; i < c1; ++i) mine += 1ull << (21 * (__popc(a.mask[keys[i] & 0xffffu]) - 1));
   // exclusive block scan of `mine`
   unsigned long long incl = mine;
-  const int lane = tid & 31, warp = tid >> 5;
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
@@ -265,6 +338,9 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     a.cand[p] = make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
     a.cidx[p] = i;
   }
+#ifdef ENUM_TIMING
+  if (tid == 0) et[7] = clock64();
+#endif
   // per 16-row scorer tile: plain (all first-of-super-node, no padding rows)
   {
     const int Rr = st->R;  // written by the last thread before the candidate section's barriers
@@ -291,7 +367,14 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     st->grp_cta[2] = st->grp_cta[1] + (cnt2 + a.cpc[2] - 1) / a.cpc[2] * a.nsl;
     st->grp_cta[3] = st->grp_cta[2] + (cnt3 + a.cpc[3] - 1) / a.cpc[3] * a.nsl;
     if (a.use_cond) cudaGraphSetConditional(a.cond, 1u);
-    if (a.tdbg) a.tdbg[size_t(st->iter) * 8 + 3] = globaltimer();
+    if (a.tdbg) a.tdbg[size_t(st->iter) * kTdbg + 3] = globaltimer();
+#ifdef ENUM_TIMING
+    et[8] = clock64();
+    if (st->iter == 100 || st->iter == 500)
+      printf("enum iter %d ns %d C %d: table pass1 %lld scan %lld emit %lld | keys %lld sort %lld out %lld group %lld tplain %lld\n",
+             st->iter, ns, C, et[1] - et[0], et[2] - et[1], et[3] - et[2], et[4] - et[3], et[5] - et[4], et[6] - et[5],
+             et[7] - et[6], et[8] - et[7]);
+#endif
   }
 }
 
@@ -309,7 +392,7 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   if (st->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int C = st->C;
-  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * 8 + 0] = globaltimer();
+  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 0] = globaltimer();
   double bs = __longlong_as_double(0x7ff0000000000000LL);
   int bi = -1;
   for (int c = tid; c < C; c += kLoopThreads) {
@@ -412,7 +495,7 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
     st->last_r = r;
     if (a.has_target && double(a.n - (ns - 1)) / double(a.n) >= a.target) st->done = 1;
     if (it + 1 >= a.cap) st->done = 1;
-    if (a.tdbg) a.tdbg[size_t(it) * 8 + 1] = globaltimer();
+    if (a.tdbg) a.tdbg[size_t(it) * kTdbg + 1] = globaltimer();
   }
 }
 

@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(128, 3) score3_kernel(S3Args a) {
     if (a.tdbg && b == 0 && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      a.tdbg[size_t(a.st->iter) * 8 + 6] = t;
+      a.tdbg[size_t(a.st->iter) * kTdbg + 6] = t;
     }
     C = a.st->C;
     R = a.st->R;

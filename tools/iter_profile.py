@@ -37,7 +37,7 @@ ctx = kr.Context(kr.HostProblem(str(path(args.case, "net.json")), str(path(args.
 cfg = kr.ReductionConfig(e_bar=args.e_bar, target_reduction=args.target)
 ctx.run_reduction(cfg)  # graph instantiation
 res = ctx.run_reduction(cfg)
-T = np.fromfile(dump, dtype=np.uint64).reshape(-1, 8).astype(np.int64)
+T = np.fromfile(dump, dtype=np.uint64).reshape(-1, 16).astype(np.int64)
 it = len(res.trace)
 L = len(res.trace[0].max_err) if it else 0
 rows = []
@@ -48,7 +48,10 @@ for i in range(1, it - 1):
     after = (nx[6] - c[1]) / 1e3  # pick end -> next score start (enum || refresh)
     C = res.trace[i].candidate_count
     ns = res.trace[i].supernode_count + 1  # before the commit
-    rows.append((i, C, ns, score, pick, after))
+    # next iteration's enum / refresh phases, relative to this pick's end
+    en = (nx[3] - c[1]) / 1e3
+    rs, rst, rwk, re0, rel = [(nx[k] - c[1]) / 1e3 for k in (4, 8, 9, 5, 10)]
+    rows.append((i, C, ns, score, pick, after, en, rs, rst, rwk, re0, rel))
 a = np.array(rows)
 print(f"{args.case}: {it} iterations, L={L}, total device {res.device_ms:.1f} ms")
 print(" iters      C_avg   ns_avg  score_us  pick_us  enum|refresh_us  Mpair-rows/us")
@@ -58,5 +61,9 @@ for b0 in range(0, len(a), args.bucket):
     print(f"{int(s[0,0]):4d}-{int(s[-1,0]):4d} {s[:,1].mean():8.0f} {s[:,2].mean():8.0f} {s[:,3].mean():9.1f} "
           f"{s[:,4].mean():8.1f} {s[:,5].mean():14.1f} {pr / s[:,3].mean() / 1e6:12.3f}")
 print(f"sum: score {a[:,3].sum()/1e3:.1f} ms, pick {a[:,4].sum()/1e3:.1f} ms, enum|refresh {a[:,5].sum()/1e3:.1f} ms")
+m = a[:, 6:].mean(axis=0)
+print(f"after pick (us, mean): enum end {m[0]:.1f} | refresh start {m[1]:.1f}, staged {m[2]:.1f}, "
+      f"walk done {m[3]:.1f}, CTA0 end {m[4]:.1f}, last CTA end {m[5]:.1f} | next score {a[:,5].mean():.1f}")
 if args.out:
-    np.savetxt(args.out, a, fmt="%.3f", delimiter="\t", header="iter\tC\tns\tscore_us\tpick_us\tafter_us")
+    np.savetxt(args.out, a, fmt="%.3f", delimiter="\t",
+               header="iter\tC\tns\tscore_us\tpick_us\tafter_us\tenum_end\tref_start\tref_staged\tref_walk\tref_end0\tref_end")
