@@ -1273,7 +1273,9 @@ struct Engine::Impl {
     while (p < x) p <<= 1;
     return p;
   }
-  size_t enum_smem() const { return pow2_at_least(std::max<size_t>(2 * prob.net.branches.size(), 1)) * sizeof(unsigned); }
+  // enumeration keys: a power-of-two sort region, then the previous sorted list
+  size_t enum_kcap() const { return pow2_at_least(std::max<size_t>(2 * prob.net.branches.size(), 1)); }
+  size_t enum_smem() const { return (enum_kcap() + 2 * prob.net.branches.size() + 1) * sizeof(unsigned); }
 
   bool device_loop_ok(const ReductionConfig& c) const {
     return !force_host_loop && c.use_delta && c.objective == Objective::magnitude && world == 1 && !profile &&
@@ -1290,6 +1292,8 @@ struct Engine::Impl {
     a.nphi = nphi;
     a.cap = n;
     a.e_bar = cfg.e_bar;
+    a.kcap = int(enum_kcap());
+    a.inc_enum = std::getenv("KRONRED_ENUM_FULL") == nullptr ? 1 : 0;
     a.nsl = s3_nsl();
     for (int k = 1; k <= 3; ++k) a.cpc[k] = kS3Slots / k;
     a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand

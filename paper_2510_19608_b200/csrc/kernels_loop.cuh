@@ -31,6 +31,8 @@ struct LoopArgs {
   LoopState* st;
   int n, nb, slack, L, nphi, cap;
   int cpc[4];          // candidates per scorer CTA for each |phi(r)| group (1..3)
+  int inc_enum;        // 1: incremental candidate list after a commit (else full rebuild)
+  int kcap;            // keys region size (power of two >= 2 nb); the previous list follows it
   int nsl;             // scenario slices per candidate group (score3), 1 otherwise
   const double* psm;   // score3 per-pair SMICE [L][ldc] (null: pcand holds per-candidate sums)
   int ldc;
@@ -68,6 +70,20 @@ struct LoopArgs {
 constexpr unsigned kPadEntry = 7u;  // rho 0, first, phase 3 (inert row)
 constexpr int kTabPadRows = 64;    // row-table padding >= largest scorer tile
 constexpr int kLoopThreads = 1024;
+constexpr int kIncCap = 512;  // incremental enumeration: largest removed / added key set
+
+// first index in the ascending array v[0..n) whose value is >= x
+__device__ __forceinline__ int lower_bound_u(const unsigned* v, int n, unsigned x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
 
 // 4-state transducer of the row-table layout: state q = rows mod 4 so far.
 // A super-node with k rows that does not fit the current block is pushed to
@@ -139,6 +155,8 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   extern __shared__ unsigned keys[];  // [pow2 >= 2n]
   __shared__ int s_cnt;
   __shared__ TabMap wmap[kLoopThreads / 32];
+  __shared__ int s_nrem, s_nnew;
+  __shared__ unsigned s_rem[kIncCap], s_nk[kIncCap], s_remk[kIncCap];
   __shared__ unsigned long long gscan[kLoopThreads / 32];
   LoopState* st = a.st;
   const int tid = threadIdx.x;
@@ -233,67 +251,154 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
 #endif
   // ---- candidates: super-node edges, both directions, filtered ------------
   if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 7] = globaltimer();
-  if (tid == 0) s_cnt = 0;
+  // After a commit (s*, r*) only the keys with an end in {s*, r*} change: r*
+  // is gone and s* owns the union of both edge sets (contracting a tree edge
+  // creates no parallel edges, and the filters depend only on the two end
+  // super-nodes). So the sorted list is the previous one minus those keys,
+  // merged with the keys of s*'s edges re-generated from the branch list. A
+  // full rebuild (generation + bitonic sort) runs on the first enumeration of
+  // a reduction and whenever either change set exceeds kIncCap.
+  const int C_old = st->C, ls = st->last_s, lr = st->last_r;
+  bool inc = a.inc_enum && st->iter > 0 && C_old > 0;
+  if (tid == 0) {
+    s_cnt = 0;
+    s_nrem = 0;
+    s_nnew = 0;
+  }
   __syncthreads();
-  // warp-aggregated slot allocation (one shared atomic per warp and direction)
-  for (int b0 = 0; b0 < a.nb; b0 += kLoopThreads) {
-    const int b = b0 + tid;
-    bool e1 = false, e2 = false;
-    unsigned k1 = 0, k2 = 0;
-    if (b < a.nb) {
-      const int x = a.sup[a.br_from[b]], y = a.sup[a.br_to[b]];
-      if (x != y) {
-        const unsigned mx = a.mask[x], my = a.mask[y];
-        e1 = y != a.slack && (my & ~mx) == 0u;
-        e2 = x != a.slack && (mx & ~my) == 0u;
-        k1 = (unsigned(x) << 16) | unsigned(y);
-        k2 = (unsigned(y) << 16) | unsigned(x);
+  unsigned* old = keys + a.kcap;  // previous sorted keys (second region)
+  if (inc) {
+    for (int i = tid; i < C_old; i += kLoopThreads) {
+      const int cs = a.cs[i], cr = a.cr[i];
+      old[i] = (unsigned(cs) << 16) | unsigned(cr);
+      if (cs == ls || cs == lr || cr == ls || cr == lr) {
+        const int slot = atomicAdd(&s_nrem, 1);
+        if (slot < kIncCap) s_rem[slot] = unsigned(i);
       }
     }
-    const unsigned lane_lt = (1u << (tid & 31)) - 1u;
-    const unsigned m1 = __ballot_sync(0xffffffffu, e1), m2 = __ballot_sync(0xffffffffu, e2);
-    const int n1 = __popc(m1), n2 = __popc(m2);
-    int base = 0;
-    if ((tid & 31) == 0 && n1 + n2 > 0) base = atomicAdd(&s_cnt, n1 + n2);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (e1) keys[base + __popc(m1 & lane_lt)] = k1;
-    if (e2) keys[base + n1 + __popc(m2 & lane_lt)] = k2;
-  }
-#ifdef ENUM_TIMING
-  if (tid == 0) et[4] = clock64();
-#endif
-  __syncthreads();
-  const int C = s_cnt;
-  if (C == 0) {
-    if (tid == 0) {
-      st->C = 0;
-      st->done = 1;
-      if (a.use_cond) cudaGraphSetConditional(a.cond, 0u);
-    }
-    return;
-  }
-  int N = 1;
-  while (N < C) N <<= 1;
-  for (int i = C + tid; i < N; i += kLoopThreads) keys[i] = 0xffffffffu;
-  __syncthreads();
-  for (int k = 2; k <= N; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < N; i += kLoopThreads) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned ki = keys[i], kl = keys[l];
-          const bool up = (i & k) == 0;
-          if ((ki > kl) == up) {
-            keys[i] = kl;
-            keys[l] = ki;
-          }
+    for (int b = tid; b < a.nb; b += kLoopThreads) {
+      const int x = a.sup[a.br_from[b]], y = a.sup[a.br_to[b]];
+      if (x != y && (x == ls || y == ls)) {
+        const unsigned mx = a.mask[x], my = a.mask[y];
+        if (y != a.slack && (my & ~mx) == 0u) {
+          const int slot = atomicAdd(&s_nnew, 1);
+          if (slot < kIncCap) s_nk[slot] = (unsigned(x) << 16) | unsigned(y);
+        }
+        if (x != a.slack && (mx & ~my) == 0u) {
+          const int slot = atomicAdd(&s_nnew, 1);
+          if (slot < kIncCap) s_nk[slot] = (unsigned(y) << 16) | unsigned(x);
         }
       }
-      __syncthreads();
+    }
+    __syncthreads();
+    inc = s_nrem <= kIncCap && s_nnew <= kIncCap;
+  }
+  int C;
+  if (inc) {
+    const int mr = s_nrem, mn = s_nnew;
+    // rank sorts of the two small sets (values are unique)
+    unsigned ri = 0u, nv = 0u;
+    int rr = 0, rn = 0;
+    if (tid < mr) {
+      ri = s_rem[tid];
+      for (int j = 0; j < mr; ++j) rr += s_rem[j] < ri ? 1 : 0;
+    }
+    if (tid < mn) {
+      nv = s_nk[tid];
+      for (int j = 0; j < mn; ++j) rn += s_nk[j] < nv ? 1 : 0;
+    }
+    __syncthreads();
+    if (tid < mr) s_rem[rr] = ri;
+    if (tid < mn) s_nk[rn] = nv;
+    __syncthreads();
+    if (tid < mr) s_remk[tid] = old[s_rem[tid]];  // removed keys, ascending
+    __syncthreads();
+    // kept key i lands at i - (removed before it) + (new keys below it);
+    // new key j at (old keys below it) - (removed keys below it) + j
+    for (int i = tid; i < C_old; i += kLoopThreads) {
+      const unsigned k = old[i];
+      const int cs = int(k >> 16), cr = int(k & 0xffffu);
+      if (cs == ls || cs == lr || cr == ls || cr == lr) continue;
+      keys[i - lower_bound_u(s_rem, mr, unsigned(i)) + lower_bound_u(s_nk, mn, k)] = k;
+    }
+    for (int j = tid; j < mn; j += kLoopThreads) {
+      const unsigned v = s_nk[j];
+      keys[lower_bound_u(old, C_old, v) - lower_bound_u(s_remk, mr, v) + j] = v;
+    }
+    C = C_old - mr + mn;
+#ifdef ENUM_TIMING
+    if (tid == 0) et[4] = et[5] = clock64();
+#endif
+    __syncthreads();
+    if (C == 0) {
+      if (tid == 0) {
+        st->C = 0;
+        st->done = 1;
+        if (a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+      }
+      return;
+    }
+  } else {
+    // warp-aggregated slot allocation (one shared atomic per warp and direction)
+    for (int b0 = 0; b0 < a.nb; b0 += kLoopThreads) {
+      const int b = b0 + tid;
+      bool e1 = false, e2 = false;
+      unsigned k1 = 0, k2 = 0;
+      if (b < a.nb) {
+        const int x = a.sup[a.br_from[b]], y = a.sup[a.br_to[b]];
+        if (x != y) {
+          const unsigned mx = a.mask[x], my = a.mask[y];
+          e1 = y != a.slack && (my & ~mx) == 0u;
+          e2 = x != a.slack && (mx & ~my) == 0u;
+          k1 = (unsigned(x) << 16) | unsigned(y);
+          k2 = (unsigned(y) << 16) | unsigned(x);
+        }
+      }
+      const unsigned lane_lt = (1u << (tid & 31)) - 1u;
+      const unsigned m1 = __ballot_sync(0xffffffffu, e1), m2 = __ballot_sync(0xffffffffu, e2);
+      const int n1 = __popc(m1), n2 = __popc(m2);
+      int base = 0;
+      if ((tid & 31) == 0 && n1 + n2 > 0) base = atomicAdd(&s_cnt, n1 + n2);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (e1) keys[base + __popc(m1 & lane_lt)] = k1;
+      if (e2) keys[base + n1 + __popc(m2 & lane_lt)] = k2;
     }
 #ifdef ENUM_TIMING
-  if (tid == 0) et[5] = clock64();
+    if (tid == 0) et[4] = clock64();
 #endif
+    __syncthreads();
+    C = s_cnt;
+    if (C == 0) {
+      if (tid == 0) {
+        st->C = 0;
+        st->done = 1;
+        if (a.use_cond) cudaGraphSetConditional(a.cond, 0u);
+      }
+      return;
+    }
+    int N = 1;
+    while (N < C) N <<= 1;
+    for (int i = C + tid; i < N; i += kLoopThreads) keys[i] = 0xffffffffu;
+    __syncthreads();
+    for (int k = 2; k <= N; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < N; i += kLoopThreads) {
+          const int l = i ^ j;
+          if (l > i) {
+            const unsigned ki = keys[i], kl = keys[l];
+            const bool up = (i & k) == 0;
+            if ((ki > kl) == up) {
+              keys[i] = kl;
+              keys[l] = ki;
+            }
+          }
+        }
+        __syncthreads();
+      }
+#ifdef ENUM_TIMING
+    if (tid == 0) et[5] = clock64();
+#endif
+  }
   for (int i = tid; i < C; i += kLoopThreads) {
     a.cs[i] = int(keys[i] >> 16);
     a.cr[i] = int(keys[i] & 0xffffu);
