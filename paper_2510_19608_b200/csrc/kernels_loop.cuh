@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   __shared__ int s_cnt;
   __shared__ TabMap wmap[kLoopThreads / 32];
   __shared__ int s_nrem, s_nnew;
+  __shared__ int s_gbase[4], s_wcnt[kLoopThreads / 32][4];
   __shared__ unsigned s_rem[kIncCap], s_nk[kIncCap], s_remk[kIncCap];
   __shared__ unsigned long long gscan[kLoopThreads / 32];
   LoopState* st = a.st;
@@ -407,41 +408,67 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
 #ifdef ENUM_TIMING
   if (tid == 0) et[6] = clock64();
 #endif
-  // ---- group by |phi(r)| (stable): packed 3 x 21-bit counters, block scan --
-  const int cch = (C + kLoopThreads - 1) / kLoopThreads;
-  const int c0 = min(C, tid * cch), c1 = min(C, c0 + cch);
+  // ---- group by |phi(r)| (stable) ----------------------------------------
+  // Rounds of one element per thread (coalesced, independent loads): group
+  // totals first (packed 3 x 21-bit counters, block reduction), then per
+  // round a warp-ballot rank, a scan of the 32 warp counts and running group
+  // bases.
   unsigned long long mine = 0;
-  for (int i = c0; i < c1; ++i) mine += 1ull << (21 * (__popc(a.mask[keys[i] & 0xffffu]) - 1));
-  // exclusive block scan of `mine`
-  unsigned long long incl = mine;
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) gscan[warp] = incl;
+  for (int i = tid; i < C; i += kLoopThreads) mine += 1ull << (21 * (__popc(a.mask[keys[i] & 0xffffu]) - 1));
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if (lane == 0) gscan[warp] = mine;
   __syncthreads();
   if (warp == 0) {
     unsigned long long w = gscan[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += v;
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (lane == 0) {
+      const int c1 = int(w & 0x1fffff), c2 = int((w >> 21) & 0x1fffff);
+      s_gbase[1] = 0;
+      s_gbase[2] = c1;
+      s_gbase[3] = c1 + c2;
     }
-    gscan[lane] = w;  // inclusive over warps
   }
   __syncthreads();
-  const unsigned long long total = gscan[kLoopThreads / 32 - 1];
-  const unsigned long long excl = incl - mine + (warp > 0 ? gscan[warp - 1] : 0ull);
-  const int cnt1 = int(total & 0x1fffff), cnt2 = int((total >> 21) & 0x1fffff);
-  int pos[4] = {0, 0, cnt1, cnt1 + cnt2};
-  pos[1] += int(excl & 0x1fffff);
-  pos[2] += int((excl >> 21) & 0x1fffff);
-  pos[3] += int((excl >> 42) & 0x1fffff);
-  for (int i = c0; i < c1; ++i) {
-    const int s = int(keys[i] >> 16), r = int(keys[i] & 0xffffu);
-    const int g = __popc(a.mask[r]);
-    const int p = pos[g]++;
-    a.cand[p] = make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
-    a.cidx[p] = i;
+  const int cnt1 = s_gbase[2], cnt2 = s_gbase[3] - s_gbase[2];
+  const unsigned lane_lt = (1u << lane) - 1u;
+  for (int r0 = 0; r0 < C; r0 += kLoopThreads) {
+    const int i = r0 + tid;
+    int s = 0, r = 0, g = 0;
+    if (i < C) {
+      s = int(keys[i] >> 16);
+      r = int(keys[i] & 0xffffu);
+      g = __popc(a.mask[r]);
+    }
+    const unsigned b1 = __ballot_sync(0xffffffffu, g == 1), b2 = __ballot_sync(0xffffffffu, g == 2),
+                   b3 = __ballot_sync(0xffffffffu, g == 3);
+    if (lane == 0) {
+      s_wcnt[warp][1] = __popc(b1);
+      s_wcnt[warp][2] = __popc(b2);
+      s_wcnt[warp][3] = __popc(b3);
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the warp counts, per group, plus the running base
+#pragma unroll
+      for (int gg = 1; gg <= 3; ++gg) {
+        const int v = s_wcnt[lane][gg];
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        s_wcnt[lane][gg] = s_gbase[gg] + x - v;
+        __syncwarp();
+        if (lane == 31) s_gbase[gg] += x;
+      }
+    }
+    __syncthreads();
+    if (i < C) {
+      const unsigned bg = g == 1 ? b1 : (g == 2 ? b2 : b3);
+      const int p = s_wcnt[warp][g] + __popc(bg & lane_lt);
+      a.cand[p] = make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
+      a.cidx[p] = i;
+    }
+    __syncthreads();  // s_wcnt is rewritten next round
   }
 #ifdef ENUM_TIMING
   if (tid == 0) et[7] = clock64();
