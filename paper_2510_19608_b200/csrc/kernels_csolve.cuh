@@ -438,6 +438,21 @@ __device__ __forceinline__ void sts2(unsigned addr, C2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// Program record (int4) at a byte offset: shared memory (32-bit address)
+// when the program is staged, global (read-only path) otherwise.
+template <bool SM>
+__device__ __forceinline__ int4 rec4(unsigned ms, const int4* g, int byteoff) {
+  if constexpr (SM) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(ms + unsigned(byteoff)));
+    return v;
+  } else {
+    return __ldg(g + (byteoff >> 4));
+  }
+}
+
 // Factor coefficient at a byte offset: shared memory (32-bit address) when
 // the program is staged, global (read-only path) otherwise.
 template <bool SM>
@@ -550,12 +565,14 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   // the index is clamped to it); a scalar step's coefficients and its own
   // forward value t_k one round ahead (the factor is read-only during the
   // sweep and x_k is written only by its own step).
+  // records by byte offset from this lane's slot of round 0
   const int4* bsl = bs + lane;
   const int4* bxl = bx + lane;
-  asm volatile("mov.b64 %0, %0;" : "+l"(bsl));
-  asm volatile("mov.b64 %0, %0;" : "+l"(bxl));
-  int4 rc = bsl[0], rx = bxl[0];
-  int4 nx = bsl[min(1, nbr) * 32], nxx = bxl[min(1, nbr) * 32];
+  unsigned ssl = SM ? unsigned(__cvta_generic_to_shared(bsl)) : 0u, sxl = SM ? unsigned(__cvta_generic_to_shared(bxl)) : 0u;
+  asm volatile("mov.b32 %0, %0;" : "+r"(ssl));
+  asm volatile("mov.b32 %0, %0;" : "+r"(sxl));
+  int4 rc = rec4<SM>(ssl, bsl, 0), rx = rec4<SM>(sxl, bxl, 0);
+  int4 nx = rec4<SM>(ssl, bsl, min(1, nbr) * 512), nxx = rec4<SM>(sxl, bxl, min(1, nbr) * 512);
   const bool sc0 = rc.x >= 0 && rx.x == 0;
   C2 aa = sc0 ? cfl<SM>(cs, cf, rc.w) : C2{0.0, 0.0}, pv = sc0 ? cfl<SM>(cs, cf, rc.y) : C2{0.0, 0.0};
   C2 t = sc0 ? lds2(xs + rc.x) : C2{0.0, 0.0};
@@ -582,7 +599,7 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
     const bool scn = nx.x >= 0 && nxx.x == 0;
     const C2 aa_n = cfl<SM>(cs, cf, scn ? nx.w : 0), pv_n = cfl<SM>(cs, cf, scn ? nx.y : 0);
     const C2 t_n = lds2(xs + (scn ? nx.x : 0));
-    const int4 nx2 = bsl[min(br + 2, nbr) * 32], nxx2 = bxl[min(br + 2, nbr) * 32];
+    const int4 nx2 = rec4<SM>(ssl, bsl, min(br + 2, nbr) * 512), nxx2 = rec4<SM>(sxl, bxl, min(br + 2, nbr) * 512);
     const bool sc = rc.x >= 0 && rx.x == 0;
     if (__all_sync(0xffffffffu, rc.x < 0 || (rx.x == 0 && rx.w == 0))) {
       // every step of the round is scalar with the single coupling to its
@@ -750,7 +767,14 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     if (wb.x < 0) nb = -1;
     int4 ra = na >= 0 ? fs[wa.x] : none, xa = na >= 0 ? fx[wa.x] : none;
     int4 rb = nb >= 0 ? fs[wb.x] : none, xb = nb >= 0 ? fx[wb.x] : none;
+#ifdef BR_TRACE
+    const long long wt0 = clock64();
+    int wsteps = 0;
+#endif
     while (na >= 0 || nb >= 0) {
+#ifdef BR_TRACE
+      ++wsteps;
+#endif
       const bool ta = na >= 0 && (nb < 0 || wa.z <= wb.z);
       const bool tb = nb >= 0 && (na < 0 || wb.z <= wa.z);
       const int4 wk = ta ? wa : wb, rc = ta ? ra : rb, rx = ta ? xa : xb;
@@ -794,6 +818,10 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
         xb = xu;
       }
     }
+#ifdef BR_TRACE
+    if (a.st && blockIdx.x == 0 && warp == 0 && (a.st->iter % 100) == 1)
+      printf("walk iter %d: %d steps, %lld cycles\n", a.st->iter, wsteps, clock64() - wt0);
+#endif
   }
   __syncwarp();  // the walk (lane 0) wrote x
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
