@@ -230,3 +230,20 @@ def test_large_feeders_first_iterations_bitwise(case):
     ctx = kr.Context(host(case))
     res = ctx.run_reduction(cfg_from_flags([f for f in meta["flags"] if f not in ("--workers", "0")]))
     assert_trace(res, case, tag)
+
+
+def test_incremental_enumeration_matches_full_rebuild(monkeypatch):
+    """The device loop's incremental candidate list (previous sorted list minus
+    the keys of the committed pair, merged with s*'s re-generated edges) gives
+    the same trajectory and scores as a full rebuild every iteration and as
+    the host-driven loop."""
+    cfg = kr.ReductionConfig(e_bar=3e-3)
+    a = kr.Context(host("c2")).run_reduction(cfg)
+    monkeypatch.setenv("KRONRED_ENUM_FULL", "1")
+    b = kr.Context(host("c2")).run_reduction(cfg)
+    key = lambda res: [(t.s, t.r, t.candidate_count, bits(t.smice)) for t in res.trace]
+    assert key(a) == key(b)
+    monkeypatch.delenv("KRONRED_ENUM_FULL")
+    monkeypatch.setenv("KRONRED_LOOP", "host")
+    c = kr.Context(host("c2")).run_reduction(cfg)
+    assert key(a) == key(c)
