@@ -282,7 +282,7 @@ def main() -> None:
     achieved = sk["flops"] / (sk["ms"] / 1e3) / 1e9 if sk["ms"] else 0.0
     roof = {"bound": "fp64", "achieved": achieved, "peak": fp64, "unit": "GFLOP/s",
             "frac": achieved / fp64 if fp64 else None, "traffic": traffic,
-            "kernel": "score_kernel", "launches": sk["launches"],
+            "kernel": "score3_kernel", "launches": sk["launches"],
             "avg_launch_us": 1e3 * sk["ms"] / max(sk["launches"], 1),
             "share_of_step": sk["ms"] / ms if ms else None,
             "algorithmic_flops_per_launch": sk["flops"] / max(sk["launches"], 1),
