@@ -247,3 +247,25 @@ def test_incremental_enumeration_matches_full_rebuild(monkeypatch):
     monkeypatch.setenv("KRONRED_LOOP", "host")
     c = kr.Context(host("c2")).run_reduction(cfg)
     assert key(a) == key(c)
+
+
+def test_c4_96_scenarios_first_iterations_bitwise(tmp_path):
+    """BASELINE configs[4] shape: the 8,381-node feeder with 96 load scenarios.
+    The library (49 MB, not committed) is regenerated with the reference
+    generator from oracle/_ref; the reference's first iterations and final
+    errors are the committed trace (tests/golden/c4L96)."""
+    import subprocess
+    from pathlib import Path
+    ref = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "kronred_ref"
+    if not ref.exists():
+        pytest.skip("oracle/_ref not built (make -C oracle)")
+    params = json.loads(path("c4L96", "params.json").read_text())
+    scen = tmp_path / "scen.csv"
+    subprocess.run([str(ref), "gen", "--n", str(params["n"]), "--seed", str(params["seed"]), "--L", str(params["L"]),
+                    "--branching", str(params["branching"]), "--net", str(tmp_path / "net.json"), "--scen", str(scen)],
+                   check=True, capture_output=True)
+    assert (tmp_path / "net.json").read_bytes() == path("c4", "net.json").read_bytes()
+    (tag, meta), = runs("c4L96").items()
+    ctx = kr.Context(kr.HostProblem(str(path("c4", "net.json")), str(scen)))
+    res = ctx.run_reduction(cfg_from_flags([f for f in meta["flags"] if f not in ("--workers", "0")]))
+    assert_trace(res, "c4L96", tag)
