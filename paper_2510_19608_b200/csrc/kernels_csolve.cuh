@@ -438,6 +438,18 @@ __device__ __forceinline__ void sts2(unsigned addr, C2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
 }
 
+#ifndef REFRESH_L2_KEEP
+#define REFRESH_L2_KEEP 1
+#endif
+// The global-program refresh (large feeders) keeps its factor and program in
+// L2 with an evict-last policy: between two refreshes the scorer streams Z
+// (1.3 GB at 8,381 nodes) through L2.
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // Program record (int4) at a byte offset: shared memory (32-bit address)
 // when the program is staged, global (read-only path) otherwise.
 template <bool SM>
@@ -449,7 +461,15 @@ __device__ __forceinline__ int4 rec4(unsigned ms, const int4* g, int byteoff) {
                  : "r"(ms + unsigned(byteoff)));
     return v;
   } else {
+#if REFRESH_L2_KEEP
+    int4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(g + (byteoff >> 4)), "l"(l2_keep_policy()));
+    return v;
+#else
     return __ldg(g + (byteoff >> 4));
+#endif
   }
 }
 
@@ -460,7 +480,14 @@ __device__ __forceinline__ C2 cfl(unsigned cs, const double2* cf, int byteoff) {
   if constexpr (SM) {
     return lds2(cs + unsigned(byteoff));
   } else {
+#if REFRESH_L2_KEEP
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(cf + (byteoff >> 4)), "l"(l2_keep_policy()));
+#else
     const double2 v = __ldg(cf + (byteoff >> 4));
+#endif
     return {v.x, v.y};
   }
 }

@@ -318,6 +318,10 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   const size_t bv_off = size_t(sl) * Ls * 2;
 
   const int nz = Gk * NL * 2 * K3;  // Z staging slots per tile (16-byte)
+#ifndef S3_Z_EVICT_FIRST
+#define S3_Z_EVICT_FIRST 1
+#endif
+  const unsigned long long zpol = S3_Z_EVICT_FIRST ? l2_evict_first_policy() : l2_evict_normal_policy();
   auto stage = [&](int j, int b) {
     const int t0 = j * K3;
     for (int i = tid; i < K3 / 4; i += P) cp_async16(tab_s(b) + 4 * i, a.tab + t0 + 4 * i);
@@ -339,7 +343,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
       const int u = i % K3;
       const int col = zcol[i / K3];
       const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-      cp_async16(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(col) * nphi + rho);
+      cp_async16_hint(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(col) * nphi + rho, zpol);
     }
   };
   // Fast staging: each thread owns at most two bv rows and one table row of
@@ -375,7 +379,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     const size_t rz = rr[2] >> 3;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (tid + q * P < nz) cp_async16(z_s(b) + zdst[q], zsrc[q] + rz);
+      if (tid + q * P < nz) cp_async16_hint(z_s(b) + zdst[q], zsrc[q] + rz, zpol);
   };
   auto form_d = [&](int b) {  // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row)
     double2* zz = z_s(b);
