@@ -460,7 +460,7 @@ struct Engine::Impl {
       g.push_back(-1);  // one exact-zero coefficient for pull-free steps
       std::vector<int> frec_of_step(size_t(std::max(h.nsteps, 1)), -1);
       auto slots = [&](const std::vector<int>& off, const std::vector<int>& steps, bool fwd, int& nrounds,
-                       std::vector<int>& recs, std::vector<int>& ext, std::vector<int>& ents) {
+                       std::vector<int>& recs, std::vector<int>& ext, std::vector<int>& ents, int lanes) {
         nrounds = 0;
         const int nl = h.nsteps ? int(off.size()) - 1 : 0;
         auto empty = [&]() {
@@ -469,8 +469,8 @@ struct Engine::Impl {
         };
         for (int lv = 0; lv < nl; ++lv) {
           const int c0 = off[size_t(lv)], cnt = off[size_t(lv) + 1] - c0;
-          for (int r0 = 0; r0 < cnt; r0 += 32, ++nrounds)
-            for (int ln = 0; ln < 32; ++ln) {
+          for (int r0 = 0; r0 < cnt; r0 += lanes, ++nrounds)
+            for (int ln = 0; ln < lanes; ++ln) {
               if (r0 + ln >= cnt) {
                 empty();
                 continue;
@@ -523,12 +523,30 @@ struct Engine::Impl {
               }
             }
         }
-        for (int ln = 0; ln < 32; ++ln) empty();  // padding round for the unconditional prefetch
+        for (int ln = 0; ln < lanes; ++ln) empty();  // padding round for the unconditional prefetch
       };
       std::vector<int> frecs, brecs, fext, bext;
       int nfr = 0, nbr = 0;
-      slots(h.fw_off, h.fw_steps, true, nfr, frecs, fext, fe2);
-      slots(h.bw_off, h.bw_steps, false, nbr, brecs, bext, be2);
+      slots(h.fw_off, h.fw_steps, true, nfr, frecs, fext, fe2, 32);
+      slots(h.bw_off, h.bw_steps, false, nbr, brecs, bext, be2, 32);
+      // A program too large for shared memory (large feeders) runs from
+      // global memory with one scenario per CTA; its backward sweep then
+      // spreads each level over kRefreshWB warps (rounds of 32 * kRefreshWB
+      // slots, a CTA barrier per round): wide levels take ~1 round, not
+      // width / 32.
+      int wb = 1;
+      {
+        const size_t est = (g.size() + 1) * 16 +
+                           (frecs.size() + fext.size() + brecs.size() + bext.size() + fe2.size() + be2.size() +
+                            size_t(nn) * 4 + 2 * h.kept.size() + 64) * 4;
+        if (est + size_t(nph) * 16 > size_t(optin_smem) - 64 && std::getenv("KRONRED_REFRESH_WB1") == nullptr) {
+          wb = kRefreshWB;
+          brecs.clear();
+          bext.clear();
+          be2.clear();
+          slots(h.bw_off, h.bw_steps, false, nbr, brecs, bext, be2, 32 * wb);
+        }
+      }
       BaseArgs& B = d.bprog;
       auto put4 = [&](const std::vector<int>& v) {
         while (bm.size() % 4) bm.push_back(0);
@@ -586,6 +604,20 @@ struct Engine::Impl {
           break;
         }
       size_t fx = fixed;
+      B.WB = 1;
+      if (wb > 1) d.bW = 0;  // global program, one scenario per CTA
+      if (d.bW == 0 && wb > 1) {
+        d.bsm = false;
+        fx = 0;
+        B.WB = wb;
+        per_warp = size_t(nph) * 16 * (B.walk >= 0 ? 2 : 1);
+        B.rhs_staged = B.walk >= 0 ? 1 : 0;
+        if (per_warp > size_t(optin_smem) - 64) {
+          per_warp = size_t(nph) * 16;
+          B.rhs_staged = 0;
+        }
+        d.bW = 1;
+      }
       if (d.bW == 0) {
         // large network: factor and program stay in global memory (read
         // through L1/L2); only the solution (and, if they fit, the staged
@@ -789,9 +821,9 @@ struct Engine::Impl {
       b.inc_r = r;
       if (profile) CK(cudaEventRecord(ev_a, stream));
       if (full.bsm)
-        base_refresh_kernel<true><<<(L + b.W - 1) / b.W, 32 * b.W, full.bsmem, stream>>>(b);
+        base_refresh_kernel<true><<<(L + b.W - 1) / b.W, 32 * b.W * b.WB, full.bsmem, stream>>>(b);
       else
-        base_refresh_kernel<false><<<(L + b.W - 1) / b.W, 32 * b.W, full.bsmem, stream>>>(b);
+        base_refresh_kernel<false><<<(L + b.W - 1) / b.W, 32 * b.W * b.WB, full.bsmem, stream>>>(b);
       launched();
       CK(cudaGetLastError());
       if (profile) {
@@ -1439,9 +1471,9 @@ struct Engine::Impl {
       CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
       enum_kernel<<<1, kLoopThreads, enum_smem(), stream2>>>(lb);
       if (full.bsm)
-        base_refresh_kernel<true><<<(L + bb.W - 1) / bb.W, 32 * bb.W, full.bsmem, stream>>>(bb);
+        base_refresh_kernel<true><<<(L + bb.W - 1) / bb.W, 32 * bb.W * bb.WB, full.bsmem, stream>>>(bb);
       else
-        base_refresh_kernel<false><<<(L + bb.W - 1) / bb.W, 32 * bb.W, full.bsmem, stream>>>(bb);
+        base_refresh_kernel<false><<<(L + bb.W - 1) / bb.W, 32 * bb.W * bb.WB, full.bsmem, stream>>>(bb);
       CK(cudaEventRecord(ev_join, stream2));
       CK(cudaStreamWaitEvent(stream, ev_join, 0));
       }

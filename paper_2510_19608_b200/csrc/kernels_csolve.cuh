@@ -384,8 +384,11 @@ __global__ void __launch_bounds__(256) csolve_warp_kernel(CSolveArgs a, int nrhs
 //
 // record int4: x = x_k | m_k<<24 | SCALAR<<29 | INLINE<<30 | EMPTY<<31,
 //              y = pinv offset, z = inline ? x_j : first entry, w = inline ? block : count
+constexpr int kRefreshWB = 8;  // warps per scenario in the global-program backward sweep
+
 struct BaseArgs {
   int nphi, ncf, nmeta, L, W;
+  int WB;                 // warps per scenario (backward sweep rounds of 32 * WB slots); 1: one warp per scenario
   int fslot, fext, nfr, bslot, bext, nbr, fent, bent, kept, nkept;  // program offsets (ints)
   const double2* cfac;
   const int* meta;
@@ -579,7 +582,7 @@ __device__ __forceinline__ void tree_forward(const BaseArgs& a, const int* M, un
 // per round.
 template <bool SM>
 __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, unsigned xs, unsigned cs, double2* x,
-                                              const double2* cf, int lane) {
+                                              const double2* cf, int lane, int wb = 1, int wsub = 0) {
   const int4* bs = reinterpret_cast<const int4*>(M + a.bslot);
   const int4* bx = reinterpret_cast<const int4*>(M + a.bext);
   const int2* be = reinterpret_cast<const int2*>(M + a.bent);
@@ -593,13 +596,15 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   // forward value t_k one round ahead (the factor is read-only during the
   // sweep and x_k is written only by its own step).
   // records by byte offset from this lane's slot of round 0
-  const int4* bsl = bs + lane;
-  const int4* bxl = bx + lane;
+  // a round is 32 * wb slots; this warp takes slots [32 wsub, 32 wsub + 32)
+  const int4* bsl = bs + wsub * 32 + lane;
+  const int4* bxl = bx + wsub * 32 + lane;
+  const int rstride = 512 * wb;  // bytes per round
   unsigned ssl = SM ? unsigned(__cvta_generic_to_shared(bsl)) : 0u, sxl = SM ? unsigned(__cvta_generic_to_shared(bxl)) : 0u;
   asm volatile("mov.b32 %0, %0;" : "+r"(ssl));
   asm volatile("mov.b32 %0, %0;" : "+r"(sxl));
   int4 rc = rec4<SM>(ssl, bsl, 0), rx = rec4<SM>(sxl, bxl, 0);
-  int4 nx = rec4<SM>(ssl, bsl, min(1, nbr) * 512), nxx = rec4<SM>(sxl, bxl, min(1, nbr) * 512);
+  int4 nx = rec4<SM>(ssl, bsl, min(1, nbr) * rstride), nxx = rec4<SM>(sxl, bxl, min(1, nbr) * rstride);
   const bool sc0 = rc.x >= 0 && rx.x == 0;
   C2 aa = sc0 ? cfl<SM>(cs, cf, rc.w) : C2{0.0, 0.0}, pv = sc0 ? cfl<SM>(cs, cf, rc.y) : C2{0.0, 0.0};
   C2 t = sc0 ? lds2(xs + rc.x) : C2{0.0, 0.0};
@@ -626,7 +631,8 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
     const bool scn = nx.x >= 0 && nxx.x == 0;
     const C2 aa_n = cfl<SM>(cs, cf, scn ? nx.w : 0), pv_n = cfl<SM>(cs, cf, scn ? nx.y : 0);
     const C2 t_n = lds2(xs + (scn ? nx.x : 0));
-    const int4 nx2 = rec4<SM>(ssl, bsl, min(br + 2, nbr) * 512), nxx2 = rec4<SM>(sxl, bxl, min(br + 2, nbr) * 512);
+    const int4 nx2 = rec4<SM>(ssl, bsl, min(br + 2, nbr) * rstride),
+               nxx2 = rec4<SM>(sxl, bxl, min(br + 2, nbr) * rstride);
     const bool sc = rc.x >= 0 && rx.x == 0;
     if (__all_sync(0xffffffffu, rc.x < 0 || (rx.x == 0 && rx.w == 0))) {
       // every step of the round is scalar with the single coupling to its
@@ -696,9 +702,10 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
     rx = nxx;
     nx = nx2;
     nxx = nxx2;
-#ifndef BR_NOSYNC
-    __syncwarp();
-#endif
+    if (wb > 1)
+      __syncthreads();  // the round's values, for every warp of the scenario
+    else
+      __syncwarp();
   }
 #ifdef BR_TRACE
   if (tr_on && lane == 0) {
@@ -725,7 +732,10 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     a.tdbg[size_t(a.st->iter) * kTdbg + 4] = t;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rhs = blockIdx.x * a.W + warp;
+  // one warp per scenario, or (WB > 1) one scenario per CTA with WB warps
+  const int WB = a.WB, slot = WB > 1 ? 0 : warp;
+  const bool lead = WB == 1 || warp == 0;  // the warp that runs the serial parts
+  const int rhs = blockIdx.x * a.W + slot;
   const int nw = min(a.W, a.L - blockIdx.x * a.W);
   const double2* cf = SM ? smem : a.cfac;
   const int* M = SM ? reinterpret_cast<const int*>(smem + a.ncf) : a.meta;
@@ -755,9 +765,9 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   mbar_wait(&bar, 0);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[0] = clock64();
   if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 8] = globaltimer_ns();
-  if (warp >= nw) return;
-  double2* x = xall + size_t(warp) * a.nphi;
-  for (int k = lane; k < a.nkept; k += 32) {
+  if (slot >= nw) return;
+  double2* x = xall + size_t(slot) * a.nphi;
+  for (int k = lane; k < a.nkept && lead; k += 32) {
     const int xe = M[a.kept + 2 * k], ki = M[a.kept + 2 * k + 1];
     const int x0 = xe & 0xffffff, m = xe >> 24;
     for (int i = 0; i < m; ++i) x[x0 + i] = a.kept_val[ki * 3 + i];
@@ -774,18 +784,18 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   const int4* fs = reinterpret_cast<const int4*>(M + a.fslot);
   const int4* fx = reinterpret_cast<const int4*>(M + a.fext);
   const int2* fe = reinterpret_cast<const int2*>(M + a.fent);
-  if (!a.inc) {
+  if (!a.inc && lead) {
     tree_forward<SM>(a, M, xs, cs, x, cf, lane);
     if (a.tfwd)  // keep the forward values for the next (incremental) refresh
       for (int r = lane; r < a.nphi; r += 32) a.tfwd[size_t(rhs) * a.nphi + r] = x[r];
-  } else if (lane == 0) {
+  } else if (a.inc && lead && lane == 0) {
     // Walk the ancestors of the two changed nodes in elimination order. The
     // two path heads keep their walk entry and step records in registers; a
     // step issues its parent's record loads before its own arithmetic, and a
     // scalar step takes its right-hand side straight from the staged copy
     // (same operations and order as tree_fwd_step).
     const int4* W = reinterpret_cast<const int4*>(M + a.walk);
-    const double2* xr = stage_rhs ? xall + size_t(a.W + warp) * a.nphi : a.iaggp + size_t(rhs) * a.nphi;
+    const double2* xr = stage_rhs ? xall + size_t(a.W + slot) * a.nphi : a.iaggp + size_t(rhs) * a.nphi;
     double2* tf = a.tfwd + size_t(rhs) * a.nphi;
     const int4 none = make_int4(-1, -1, 0x7fffffff, -1);
     int na = a.st ? a.st->last_s : a.inc_s, nb = a.st ? a.st->last_r : a.inc_r;
@@ -850,12 +860,15 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
       printf("walk iter %d: %d steps, %lld cycles\n", a.st->iter, wsteps, clock64() - wt0);
 #endif
   }
-  __syncwarp();  // the walk (lane 0) wrote x
+  if (WB > 1)
+    __syncthreads();  // the lead warp's forward values
+  else
+    __syncwarp();  // the walk (lane 0) wrote x
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[2] = clock64();
   if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 9] = globaltimer_ns();
-  tree_backward<SM>(a, M, xs, cs, x, cf, lane);
+  tree_backward<SM>(a, M, xs, cs, x, cf, lane, WB, WB > 1 ? warp : 0);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
-  for (int r = lane; r < a.nphi; r += 32) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
+  for (int r = WB > 1 ? tid : lane; r < a.nphi; r += 32 * WB) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
   if (a.tdbg && blockIdx.x == 0 && tid == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
