@@ -351,7 +351,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   // the whole item), so the column sources are resolved once and the table
   // entries are prefetched raw one tile ahead: no dependent load in front of a
   // cp.async, and the prefetch is not consumed until the next tile.
-  const bool fst = bv_fixed && (P % K3) == 0 && 2 * bv_du >= K3 && nz <= 4 * P;
+  const bool fst = bv_fixed && (P % K3) == 0 && 2 * bv_du >= K3;
   const int u_a = bv_u0, u_b = bv_u0 + bv_du, u_z = tid % K3;
   const double2* zsrc[4];
   int zdst[4];
@@ -380,6 +380,9 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (tid + q * P < nz) cp_async16_hint(z_s(b) + zdst[q], zsrc[q] + rz, zpol);
+    // small CTAs (few scenarios): the remaining slots, same table row (P % K3 == 0)
+    for (int i = tid + 4 * P; i < nz; i += P)
+      cp_async16_hint(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(zcol[i / K3]) * nphi + rz, zpol);
   };
   auto form_d = [&](int b) {  // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row)
     double2* zz = z_s(b);
