@@ -597,6 +597,11 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   // sweep and x_k is written only by its own step).
   // records by byte offset from this lane's slot of round 0
   // a round is 32 * wb slots; this warp takes slots [32 wsub, 32 wsub + 32)
+  // (multi-warp rounds only with the global program: a compile-time 1 otherwise)
+  if constexpr (SM) {
+    wb = 1;
+    wsub = 0;
+  }
   const int4* bsl = bs + wsub * 32 + lane;
   const int4* bxl = bx + wsub * 32 + lane;
   const int rstride = 512 * wb;  // bytes per round
@@ -614,6 +619,7 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   for (int i = 0; i < 80; ++i) tr_b[i] = tr_c[i] = 0;
   const bool tr_on = a.dbg && blockIdx.x == 0 && threadIdx.x < 32;
 #endif
+#pragma unroll 2
   for (int br = 0; br < nbr; ++br) {
 #ifdef BR_TRACE
     if (tr_on && br < 80) {
@@ -795,15 +801,19 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     // scalar step takes its right-hand side straight from the staged copy
     // (same operations and order as tree_fwd_step).
     const int4* W = reinterpret_cast<const int4*>(M + a.walk);
+    // shared-space bases of the walk table and the forward records (program staged)
+    const unsigned wsa = SM ? unsigned(__cvta_generic_to_shared(W)) : 0u;
+    const unsigned fsa = SM ? unsigned(__cvta_generic_to_shared(fs)) : 0u;
+    const unsigned fxa = SM ? unsigned(__cvta_generic_to_shared(fx)) : 0u;
     const double2* xr = stage_rhs ? xall + size_t(a.W + slot) * a.nphi : a.iaggp + size_t(rhs) * a.nphi;
     double2* tf = a.tfwd + size_t(rhs) * a.nphi;
     const int4 none = make_int4(-1, -1, 0x7fffffff, -1);
     int na = a.st ? a.st->last_s : a.inc_s, nb = a.st ? a.st->last_r : a.inc_r;
-    int4 wa = na >= 0 ? W[na] : none, wb = nb >= 0 ? W[nb] : none;
+    int4 wa = na >= 0 ? rec4<SM>(wsa, W, na * 16) : none, wb = nb >= 0 ? rec4<SM>(wsa, W, nb * 16) : none;
     if (wa.x < 0) na = -1;  // kept (slack): no forward step
     if (wb.x < 0) nb = -1;
-    int4 ra = na >= 0 ? fs[wa.x] : none, xa = na >= 0 ? fx[wa.x] : none;
-    int4 rb = nb >= 0 ? fs[wb.x] : none, xb = nb >= 0 ? fx[wb.x] : none;
+    int4 ra = na >= 0 ? rec4<SM>(fsa, fs, wa.x * 16) : none, xa = na >= 0 ? rec4<SM>(fxa, fx, wa.x * 16) : none;
+    int4 rb = nb >= 0 ? rec4<SM>(fsa, fs, wb.x * 16) : none, xb = nb >= 0 ? rec4<SM>(fxa, fx, wb.x * 16) : none;
 #ifdef BR_TRACE
     const long long wt0 = clock64();
     int wsteps = 0;
@@ -815,11 +825,17 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
       const bool ta = na >= 0 && (nb < 0 || wa.z <= wb.z);
       const bool tb = nb >= 0 && (na < 0 || wb.z <= wa.z);
       const int4 wk = ta ? wa : wb, rc = ta ? ra : rb, rx = ta ? xa : xb;
-      const int4 wu = wk.y >= 0 ? W[wk.y] : none;  // the parent's walk entry, in flight during the step
+      const int4 wu = wk.y >= 0 ? rec4<SM>(wsa, W, wk.y * 16) : none;  // the parent's walk entry
       const int xk = rc.x >> 4;
+      int4 ru = none, xu = none;  // the parent's step records, issued behind this step's operand loads
+      const bool upok = wk.y >= 0;
       if (rc.x >= 0 && rc.z >= 0) {
         const C2 b0 = ld2(xr + xk), tj = lds2(xs + rc.z), t1 = lds2(xs + rx.x);
         const C2 aa = cfl<SM>(cs, cf, rc.w), pv = cfl<SM>(cs, cf, rc.y), a1 = cfl<SM>(cs, cf, rx.y);
+        if (upok && wu.x >= 0) {
+          ru = rec4<SM>(fsa, fs, wu.x * 16);
+          xu = rec4<SM>(fxa, fx, wu.x * 16);
+        }
         const C2 u0 = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, tj));
         const C2 u1 = dev::cadd(C2{0.0, 0.0}, dev::cmul(a1, t1));
         C2 bb = dev::csub(dev::csub(b0, u0), u1);
@@ -841,7 +857,10 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
         for (int i = 0; i < mk; ++i) tf[xk + i] = x[xk + i];
       }
       const int up = wk.y >= 0 && wu.x >= 0 ? wk.y : -1;  // stop below kept nodes
-      const int4 ru = up >= 0 ? fs[wu.x] : none, xu = up >= 0 ? fx[wu.x] : none;
+      if (up >= 0 && !(rc.x >= 0 && rc.z >= 0)) {
+        ru = rec4<SM>(fsa, fs, wu.x * 16);
+        xu = rec4<SM>(fxa, fx, wu.x * 16);
+      }
       if (ta) {
         na = up;
         wa = wu;
