@@ -3,6 +3,9 @@
 // marshalling around the device Engine. Exceptions map to status codes the way
 // the reference CLI maps them to exit codes (main.cpp:234-246).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -282,11 +285,14 @@ void load_scenarios_from_host(Engine* eng, const Problem& p, const krg_host_prob
                        std::vector<double>(size_t(L) * 6 * size_t(hp.net.size()), 0.0));
     eng->pq_to_currents(hp.pq_loads, inj, volt);
   } else {
+    // current mode: V-hat = solve(I-hat) on the device (the engine keeps both)
     inj = hp.inj;
     zero_invalid(hp.net, inj, L);
     eng->set_scenarios(hp.ids, inj, {});
     volt.resize(inj.size());
     eng->scenario_voltages(volt.data());
+    check_residual(p, inj, volt, hp.ids);
+    return;
   }
   check_residual(p, inj, volt, hp.ids);
   eng->set_scenarios(hp.ids, inj, volt);
@@ -561,9 +567,19 @@ int krg_create_from_host(const krg_host_problem* hp, int32_t device, krg_ctx** o
 
 int krg_reload_from_host(krg_ctx* ctx, const krg_host_problem* hp) {
   KRG_TRY
+  const bool tr = std::getenv("KRONRED_RELOAD_TRACE") != nullptr;  // tuning aid: phase times
+  const auto t0 = std::chrono::steady_clock::now();
   Problem p = base_problem(hp->net);
+  const auto t1 = std::chrono::steady_clock::now();
   ctx->eng->reload(p);
+  const auto t2 = std::chrono::steady_clock::now();
   load_scenarios_from_host(ctx->eng.get(), p, *hp);
+  const auto t3 = std::chrono::steady_clock::now();
+  if (tr) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "reload: assembly %.2f ms, refactorize %.2f ms, scenarios %.2f ms\n", ms(t0, t1), ms(t1, t2),
+                 ms(t2, t3));
+  }
   return KRG_OK;
   KRG_CATCH
 }

@@ -225,6 +225,7 @@ struct Engine::Impl {
     return P;
   }
   double* h_best = nullptr;    // pinned [2 + L]
+  size_t h_best_n = 0;
   // multi-GPU
   int rank = 0, world = 1;
   krg_exchange_fn xfn = nullptr;
@@ -975,8 +976,11 @@ struct Engine::Impl {
     CK(cudaMemset(d_grpdone.p, 0, d_grpdone.n * sizeof(int)));
     d_pcand.alloc(size_t(2 * n));
     d_best.alloc(size_t(2 + L));
-    if (h_best) cudaFreeHost(h_best);
-    CK(cudaMallocHost(&h_best, sizeof(double) * size_t(2 + L)));
+    if (!h_best || h_best_n < size_t(2 + L)) {  // pinned readback slot, kept across reloads
+      if (h_best) cudaFreeHost(h_best);
+      CK(cudaMallocHost(&h_best, sizeof(double) * size_t(2 + L)));
+      h_best_n = size_t(2 + L);
+    }
   }
 
   ~Impl() {

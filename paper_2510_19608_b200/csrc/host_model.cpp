@@ -288,17 +288,21 @@ BlockAdmittance assemble_admittance(const Network& net) {
     Mat3c& tt2 = y.block(b.to, b.to);
     for (int k = 0; k < 9; ++k) tt2.m[size_t(k)] += b.shunt_to.m[size_t(k)];
   }
+  // mask every stored block to present phases (grid_model.cpp:36-50); only
+  // the row's stored blocks are visited (O(blocks), not O(n^2) lookups)
+  std::vector<int> cols;
   for (int i = 0; i < n; ++i) {
     const PhaseMask mi = net.nodes[size_t(i)].phases;
-    for (int j = 0; j < n; ++j) {
-      const Mat3c* blk = y.find(i, j);
-      if (blk == nullptr) continue;
+    cols.clear();
+    for (const auto& kv : y.row(i)) cols.push_back(kv.first);
+    for (const int j : cols) {
+      Mat3c& blk = y.block(i, j);
       const PhaseMask mj = net.nodes[size_t(j)].phases;
       Mat3c masked;
       for (int r = 0; r < 3; ++r)
         for (int c = 0; c < 3; ++c)
-          if (mi.has(r) && mj.has(c)) masked(r, c) = (*blk)(r, c);
-      y.block(i, j) = masked;
+          if (mi.has(r) && mj.has(c)) masked(r, c) = blk(r, c);
+      blk = masked;
     }
   }
   for (int i = 0; i < n; ++i) {
