@@ -499,18 +499,20 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   }
   // the last slice CTA of a candidate group reduces its candidates over the
   // scenarios (threadfence reduction: counters reset themselves)
+  // (the CTA barrier orders every thread's stores before thread 0's
+  // release-acquire add at device scope; the winner's barrier orders its
+  // acquire before every thread's loads)
   __shared__ int s_last;
-  __threadfence();
   __syncthreads();
   const int grp = (local / a.nsl) + g_base_group;
   if (tid == 0) {
-    const int old = atomicAdd(a.grp_done + grp, 1);
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.grp_done + grp) : "memory");
     s_last = old == a.nsl - 1;
     if (s_last) a.grp_done[grp] = 0;
   }
   __syncthreads();
   if (s_last) {
-    __threadfence();
     // stage the group's per-pair results in shared memory (all threads, L2
     // reads), then one thread per candidate sums in scenario order
     double* ssm = smd;                       // [Gk][L]
