@@ -1361,6 +1361,22 @@ struct Engine::Impl {
     return a;
   }
 
+  bool pdl = std::getenv("KRONRED_NO_PDL") == nullptr;
+  template <class... P, class... A>
+  void launch_dep(bool on, void (*k)(P...), dim3 g, dim3 b, size_t smem, cudaStream_t st, A... args) {
+    cudaLaunchConfig_t c{};
+    c.gridDim = g;
+    c.blockDim = b;
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    c.attrs = at;
+    c.numAttrs = on ? 1 : 0;
+    CK(cudaLaunchKernelEx(&c, k, args...));
+  }
+
   // After begin(): runs every iteration on the device (one graph launch with
   // a conditional WHILE node) and returns the committed trace.
   void run_device_loop(std::vector<int>& tr_s, std::vector<int>& tr_r, std::vector<int>& tr_c,
@@ -1470,14 +1486,18 @@ struct Engine::Impl {
       const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
       for (int u = 0; u < kLoopUnroll; ++u) {
       score3_kernel<<<grid3, s3_threads(), sm3, stream>>>(q);
-      pick_commit_kernel<<<1, kLoopThreads, 0, stream>>>(lb);
+      // pick and refresh follow their stream predecessor by programmatic
+      // dependent launch (launch overlapped with the predecessor's tail; each
+      // waits on griddepcontrol before reading its results)
+      launch_dep(pdl, pick_commit_kernel, dim3(1), dim3(kLoopThreads), 0, stream, lb);
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
       enum_kernel<<<1, kLoopThreads, enum_smem(), stream2>>>(lb);
+      const dim3 rg((L + bb.W - 1) / bb.W), rb(32 * bb.W * bb.WB);
       if (full.bsm)
-        base_refresh_kernel<true><<<(L + bb.W - 1) / bb.W, 32 * bb.W * bb.WB, full.bsmem, stream>>>(bb);
+        launch_dep(pdl, base_refresh_kernel<true>, rg, rb, size_t(full.bsmem), stream, bb);
       else
-        base_refresh_kernel<false><<<(L + bb.W - 1) / bb.W, 32 * bb.W * bb.WB, full.bsmem, stream>>>(bb);
+        launch_dep(pdl, base_refresh_kernel<false>, rg, rb, size_t(full.bsmem), stream, bb);
       CK(cudaEventRecord(ev_join, stream2));
       CK(cudaStreamWaitEvent(stream, ev_join, 0));
       }

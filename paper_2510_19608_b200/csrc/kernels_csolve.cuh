@@ -29,6 +29,9 @@ enum CMode { CM_FULL = 0, CM_BASE = 1, CM_ZCOL = 2 };
 // table done, 8 refresh staged (CTA 0), 9 refresh walk done (CTA 0), 10 last
 // refresh CTA end
 constexpr int kTdbg = 16;
+// Programmatic dependent launch: wait for the preceding kernel's results (a
+// no-op when launched without the attribute)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -731,6 +734,7 @@ template <bool SM>
 __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   extern __shared__ __align__(16) double2 smem[];
   __shared__ unsigned long long bar;
+  griddep_wait();
   if (a.st && a.st->done) return;
   if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;

@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   __shared__ double ss[32];
   __shared__ int si[32];
   __shared__ int s_pos;
+  griddep_wait();
   LoopState* st = a.st;
   if (st->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
