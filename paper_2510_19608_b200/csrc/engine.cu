@@ -1362,6 +1362,7 @@ struct Engine::Impl {
   }
 
   bool pdl = std::getenv("KRONRED_NO_PDL") == nullptr;
+  bool pdl_score = std::getenv("KRONRED_PDL_SCORE") != nullptr;
   template <class... P, class... A>
   void launch_dep(bool on, void (*k)(P...), dim3 g, dim3 b, size_t smem, cudaStream_t st, A... args) {
     cudaLaunchConfig_t c{};
@@ -1485,7 +1486,7 @@ struct Engine::Impl {
       const int items_max = ((2 * nb + 4) / 5 + 3) * s3_nsl();
       const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
       for (int u = 0; u < kLoopUnroll; ++u) {
-      score3_kernel<<<grid3, s3_threads(), sm3, stream>>>(q);
+      launch_dep(pdl && pdl_score, score3_kernel, dim3(grid3), dim3(s3_threads()), sm3, stream, q);
       // pick and refresh follow their stream predecessor by programmatic
       // dependent launch (launch overlapped with the predecessor's tail; each
       // waits on griddepcontrol before reading its results)

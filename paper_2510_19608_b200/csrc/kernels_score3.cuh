@@ -543,6 +543,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
 __global__ void __launch_bounds__(128, 3) score3_kernel(S3Args a) {
   extern __shared__ double sm_dyn[];
   const int b = blockIdx.x;
+  griddep_wait();
   int C = a.C, R = a.R;
   const int* gs = a.grp_start;
   const int* gc = a.grp_cta;
