@@ -549,6 +549,21 @@ struct Engine::Impl {
         }
       }
       BaseArgs& B = d.bprog;
+      {
+        // first backward round of an all-scalar suffix (tree_backward's tight loop)
+        const int lanes = int(brecs.size() / 4) / std::max(nbr + 1, 1);
+        int bf = nbr;
+        for (int r = nbr - 1; r >= 0; --r) {
+          bool fast = true;
+          for (int l = 0; l < lanes && fast; ++l) {
+            const size_t q = size_t(r * lanes + l) * 4;
+            fast = brecs[q] < 0 || (bext[q] == 0 && bext[q + 3] == 0);
+          }
+          if (!fast) break;
+          bf = r;
+        }
+        B.bfast = std::getenv("KRONRED_NO_BFAST") ? nbr : bf;
+      }
       auto put4 = [&](const std::vector<int>& v) {
         while (bm.size() % 4) bm.push_back(0);
         const int o = int(bm.size());

@@ -392,6 +392,7 @@ constexpr int kRefreshWB = 8;  // warps per scenario in the global-program backw
 struct BaseArgs {
   int nphi, ncf, nmeta, L, W;
   int WB;                 // warps per scenario (backward sweep rounds of 32 * WB slots); 1: one warp per scenario
+  int bfast;              // first backward round from which every round is scalar single-coupling only
   int fslot, fext, nfr, bslot, bext, nbr, fent, bent, kept, nkept;  // program offsets (ints)
   const double2* cfac;
   const int* meta;
@@ -622,8 +623,10 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   for (int i = 0; i < 80; ++i) tr_b[i] = tr_c[i] = 0;
   const bool tr_on = a.dbg && blockIdx.x == 0 && threadIdx.x < 32;
 #endif
+  const int bfast = min(a.bfast, nbr);
+  int br = 0;
 #pragma unroll 2
-  for (int br = 0; br < nbr; ++br) {
+  for (; br < bfast; ++br) {
 #ifdef BR_TRACE
     if (tr_on && br < 80) {
       tr_g[br] = __ballot_sync(0xffffffffu, rc.x >= 0 && rx.x != 0);
@@ -713,6 +716,29 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
     nxx = nxx2;
     if (wb > 1)
       __syncthreads();  // the round's values, for every warp of the scenario
+    else
+      __syncwarp();
+  }
+  // Suffix of all-scalar rounds (host-checked: every slot empty or a scalar
+  // step with its single coupling): no vote, no extension records.
+#pragma unroll 2
+  for (; br < nbr; ++br) {
+    const C2 xj = lds2(xs + (rc.x >= 0 ? rc.z : 0));
+    const bool scn = nx.x >= 0;
+    const C2 aa_n = cfl<SM>(cs, cf, scn ? nx.w : 0), pv_n = cfl<SM>(cs, cf, scn ? nx.y : 0);
+    const C2 t_n = lds2(xs + (scn ? nx.x : 0));
+    const int4 nx2 = rec4<SM>(ssl, bsl, min(br + 2, nbr) * rstride);
+    if (rc.x >= 0) {
+      const C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj));
+      sts2(xs + rc.x, dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc))));
+    }
+    aa = aa_n;
+    pv = pv_n;
+    t = t_n;
+    rc = nx;
+    nx = nx2;
+    if (wb > 1)
+      __syncthreads();
     else
       __syncwarp();
   }
