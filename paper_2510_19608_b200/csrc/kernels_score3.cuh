@@ -384,15 +384,30 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     for (int i = tid + 4 * P; i < nz; i += P)
       cp_async16_hint(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(zcol[i / K3]) * nphi + rz, zpol);
   };
-  auto form_d = [&](int b) {  // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row)
+  // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row); each
+  // thread's element offsets are fixed for the item (at most two per thread
+  // for 128-thread CTAs: both pairs loaded before either difference)
+  const int nd = Gk * NL * K3;
+  auto fd_off = [&](int i) {
+    const int col2 = i / K3, u = i - col2 * K3;
+    const int g = col2 / NL;  // candidate: its block starts at g * (NL * 2 * K3 + 1)
+    return g * (NL * 2 * K3 + 1) + (col2 - g * NL) * 2 * K3 + u;
+  };
+  const bool fd2 = nd <= 2 * P;
+  const int fdo0 = fd_off(min(tid, nd - 1)), fdo1 = fd_off(min(tid + P, nd - 1));
+  const bool fdv0 = tid < nd, fdv1 = tid + P < nd;
+  auto form_d = [&](int b) {
     double2* zz = z_s(b);
-    const int nd = Gk * NL * K3;
+    if (fd2) {
+      const double2 za0 = zz[fdo0], zr0 = zz[fdo0 + K3], za1 = zz[fdo1], zr1 = zz[fdo1 + K3];
+      if (fdv0) zz[fdo0] = make_double2(dev::dsub(za0.x, zr0.x), dev::dsub(za0.y, zr0.y));
+      if (fdv1) zz[fdo1] = make_double2(dev::dsub(za1.x, zr1.x), dev::dsub(za1.y, zr1.y));
+      return;
+    }
     for (int i = tid; i < nd; i += P) {
-      const int col2 = i / K3, u = i - col2 * K3;
-      const int g = col2 / NL;  // candidate: its block starts at g * (NL * 2 * K3 + 1)
-      double2* zc = zz + g * (NL * 2 * K3 + 1) + (col2 - g * NL) * 2 * K3;
-      const double2 za = zc[u], zr = zc[K3 + u];
-      zc[u] = make_double2(dev::dsub(za.x, zr.x), dev::dsub(za.y, zr.y));
+      double2* zc = zz + fd_off(i);
+      const double2 za = zc[0], zr = zc[K3];
+      zc[0] = make_double2(dev::dsub(za.x, zr.x), dev::dsub(za.y, zr.y));
     }
   };
 
