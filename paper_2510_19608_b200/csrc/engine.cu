@@ -1861,8 +1861,8 @@ void Engine::loop_base(double* out) {
   for (int r = 0; r < I.nphi; ++r)
     for (int l = 0; l < I.L; ++l) {
       const size_t o = (size_t(l) * 3 * I.n + size_t(I.prow_node[size_t(r)]) * 3 + I.prow_phase[size_t(r)]) * 2;
-      out[o] = bv[(size_t(r) * I.L + l) * 2].x;
-      out[o + 1] = bv[(size_t(r) * I.L + l) * 2].y;
+      out[o] = bv[bv_base(size_t(r), I.L, l)].x;
+      out[o + 1] = bv[bv_base(size_t(r), I.L, l)].y;
     }
 }
 

@@ -29,6 +29,11 @@ enum CMode { CM_FULL = 0, CM_BASE = 1, CM_ZCOL = 2 };
 // table done, 8 refresh staged (CTA 0), 9 refresh walk done (CTA 0), 10 last
 // refresh CTA end
 constexpr int kTdbg = 16;
+// base values and cluster bounds of present row r, scenario l: one row holds
+// the L base values, then the L bounds ({min, max} of the member magnitudes),
+// so a scenario slice of either is one contiguous run
+__host__ __device__ __forceinline__ size_t bv_base(size_t r, int L, int l) { return r * 2 * size_t(L) + size_t(l); }
+__host__ __device__ __forceinline__ size_t bv_bnd(size_t r, int L, int l) { return r * 2 * size_t(L) + size_t(L + l); }
 // Programmatic dependent launch: wait for the preceding kernel's results (a
 // no-op when launched without the attribute)
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(256) csolve_kernel(CSolveArgs a) {
   }
   // outputs
   if (MODE == CM_BASE) {
-    for (int r = tid; r < P.nphi; r += nt) a.base[(size_t(r) * a.L + rhs) * 2] = x[r];
+    for (int r = tid; r < P.nphi; r += nt) a.base[bv_base(size_t(r), a.L, rhs)] = x[r];
   } else if (MODE == CM_ZCOL) {
     double2* zc = a.zout + size_t(a.col0 + rhs) * P.nphi;
     for (int r = tid; r < P.nphi; r += nt) st2(zc + r, dev::csub(ld2(x + r), ld2(a.v0p + r)));
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(256) csolve_warp_kernel(CSolveArgs a, int nrhs
   }
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
   if (MODE == CM_BASE) {
-    for (int r = lane; r < P.nphi; r += 32) a.base[(size_t(r) * a.L + rhs) * 2] = x[r];
+    for (int r = lane; r < P.nphi; r += 32) a.base[bv_base(size_t(r), a.L, rhs)] = x[r];
   } else if (MODE == CM_ZCOL) {
     double2* zc = a.zout + size_t(a.col0 + rhs) * P.nphi;
     for (int r = lane; r < P.nphi; r += 32) st2(zc + r, dev::csub(ld2(x + r), ld2(a.v0p + r)));
@@ -917,7 +922,7 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 9] = globaltimer_ns();
   tree_backward<SM>(a, M, xs, cs, x, cf, lane, WB, WB > 1 ? warp : 0);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
-  for (int r = WB > 1 ? tid : lane; r < a.nphi; r += 32 * WB) a.bv[(size_t(r) * a.L + rhs) * 2] = x[r];
+  for (int r = WB > 1 ? tid : lane; r < a.nphi; r += 32 * WB) a.bv[bv_base(size_t(r), a.L, rhs)] = x[r];
   if (a.tdbg && blockIdx.x == 0 && tid == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -598,8 +598,8 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
       if ((ms >> p) & 1u) st2(a.iaggp + size_t(l) * a.nphi + rs0 + popc_below(ms, p), sum);
       if ((mr >> p) & 1u) {
         a.iaggp[size_t(l) * a.nphi + rr0 + popc_below(mr, p)] = make_double2(0.0, 0.0);
-        double2* dst = a.bv + (size_t(rs0 + popc_below(ms, p)) * L + l) * 2 + 1;
-        const double2 bb = a.bv[(size_t(rr0 + popc_below(mr, p)) * L + l) * 2 + 1];
+        double2* dst = a.bv + bv_bnd(size_t(rs0 + popc_below(ms, p)), L, l);
+        const double2 bb = a.bv[bv_bnd(size_t(rr0 + popc_below(mr, p)), L, l)];
         const double2 cur = *dst;
         *dst = make_double2(dmin(cur.x, bb.x), dmax(cur.y, bb.y));
       }

@@ -290,7 +290,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     for (int ph = 0; ph < 3; ++ph) {
       if (!((mr >> ph) & 1u)) continue;
       const int rr = rr0 + popc_below(mr, ph);
-      const double2 bnd = a.bv[(size_t(rr) * L + l) * 2 + 1];
+      const double2 bnd = a.bv[bv_bnd(size_t(rr), L, l)];
       if (ph == 0) { rlo0 = bnd.x; rhi0 = bnd.y; }
       if (ph == 1) { rlo1 = bnd.x; rhi1 = bnd.y; }
       if (ph == 2) { rlo2 = bnd.x; rhi2 = bnd.y; }
@@ -314,8 +314,11 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   const int nsc = min(Ls, L - sl * Ls);  // scenarios of this slice
   const bool bv_fixed = (P % RS) == 0;
   const int bv_ch = tid % RS, bv_u0 = tid / RS, bv_du = P / RS;
-  const int bv_dst = (bv_ch & 1) * Ls + (bv_ch >> 1);  // shared row layout [base x Ls][bounds x Ls]
-  const size_t bv_off = size_t(sl) * Ls * 2;
+  // a row's slice: Ls base values, then Ls bounds, both in global (row-planar
+  // bv, bv_base/bv_bnd) and in shared memory
+  const int bv_dst = bv_ch;
+  const size_t bv_off = size_t(bv_ch / Ls) * L + size_t(sl) * Ls + size_t(bv_ch % Ls);
+  const bool bv_in = (bv_ch % Ls) < nsc;
 
   const int nz = Gk * NL * 2 * K3;  // Z staging slots per tile (16-byte)
 #ifndef S3_Z_EVICT_FIRST
@@ -326,17 +329,18 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     const int t0 = j * K3;
     for (int i = tid; i < K3 / 4; i += P) cp_async16(tab_s(b) + 4 * i, a.tab + t0 + 4 * i);
     if (bv_fixed) {
-      if (bv_ch < 2 * nsc)
+      if (bv_in)
         for (int u = bv_u0; u < K3; u += bv_du) {
           const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-          cp_async16(bv_s(b) + size_t(u) * RS + bv_dst, a.bv + rho * 2 * L + bv_off + bv_ch);
+          cp_async16(bv_s(b) + size_t(u) * RS + bv_dst, a.bv + rho * 2 * L + bv_off);
         }
     } else {
       for (int i = tid; i < K3 * RS; i += P) {
         const int u = i / RS, ch = i - u * RS;
-        if (ch >= 2 * nsc) continue;
+        if (ch % Ls >= nsc) continue;
         const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-        cp_async16(bv_s(b) + size_t(u) * RS + (ch & 1) * Ls + (ch >> 1), a.bv + rho * 2 * L + bv_off + ch);
+        cp_async16(bv_s(b) + size_t(u) * RS + ch,
+                   a.bv + rho * 2 * L + size_t(ch / Ls) * L + size_t(sl) * Ls + size_t(ch % Ls));
       }
     }
     for (int i = tid; i < nz; i += P) {
@@ -370,11 +374,11 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   auto stage_fast = [&](int j, int b, const unsigned (&rr)[3]) {
     const int t0 = j * K3;
     if (tid < K3 / 4) cp_async16(tab_s(b) + 4 * tid, a.tab + t0 + 4 * tid);
-    if (bv_ch < 2 * nsc) {
+    if (bv_in) {
       if (u_a < K3)
-        cp_async16(bv_s(b) + size_t(u_a) * RS + bv_dst, a.bv + size_t(rr[0] >> 3) * 2 * L + bv_off + bv_ch);
+        cp_async16(bv_s(b) + size_t(u_a) * RS + bv_dst, a.bv + size_t(rr[0] >> 3) * 2 * L + bv_off);
       if (u_b < K3)
-        cp_async16(bv_s(b) + size_t(u_b) * RS + bv_dst, a.bv + size_t(rr[1] >> 3) * 2 * L + bv_off + bv_ch);
+        cp_async16(bv_s(b) + size_t(u_b) * RS + bv_dst, a.bv + size_t(rr[1] >> 3) * 2 * L + bv_off);
     }
     const size_t rz = rr[2] >> 3;
 #pragma unroll
