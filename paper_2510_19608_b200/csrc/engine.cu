@@ -144,7 +144,10 @@ enum IntArr {
 };
 
 constexpr int kTabPad = kTabPadRows;
-constexpr int kLoopUnroll = 4;  // loop iterations per conditional-graph body  // row-table padding >= largest scorer tile (S*4 rows)
+#ifndef KRONRED_LOOP_UNROLL
+#define KRONRED_LOOP_UNROLL 8
+#endif
+constexpr int kLoopUnroll = KRONRED_LOOP_UNROLL;  // loop iterations per conditional-graph body
 
 struct Engine::Impl {
   Problem prob;
