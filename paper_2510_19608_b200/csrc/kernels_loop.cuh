@@ -519,6 +519,7 @@ __device__ __forceinline__ bool loop_better(double s1, int i1, double s2, int i2
 __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   __shared__ double ss[32];
   __shared__ int si[32];
+  __shared__ unsigned sk[32];
   __shared__ int s_pos;
   griddep_wait();
   LoopState* st = a.st;
@@ -526,53 +527,69 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int C = st->C;
   if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 0] = globaltimer();
+  // the commit's first reads (super-node map and active list, which only this
+  // kernel writes) are issued ahead of the argmin
+  const int sup0 = tid < a.n ? a.sup[tid] : -1;
+  const int sn0 = tid < st->ns ? a.sn[tid] : -1;
+  // argmin with the candidate's (s, r) carried along (no dependent load after it)
   double bs = __longlong_as_double(0x7ff0000000000000LL);
   int bi = -1;
+  unsigned bk = 0u;
   for (int c = tid; c < C; c += kLoopThreads) {
     const double v = a.psm ? s3_candidate(a.psm, a.pmaxerr, c, a.L, a.ldc, a.e_bar) : a.pcand[c];
+    const unsigned key = (unsigned(a.cs[c]) << 16) | unsigned(a.cr[c]);
     if (!(v < 0.0) && loop_better(v, c, bs, bi)) {
       bs = v;
       bi = c;
+      bk = key;
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const double os = __shfl_down_sync(0xffffffffu, bs, o);
     const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+    const unsigned ok = __shfl_down_sync(0xffffffffu, bk, o);
     if (loop_better(os, oi, bs, bi)) {
       bs = os;
       bi = oi;
+      bk = ok;
     }
   }
   if (lane == 0) {
     ss[warp] = bs;
     si[warp] = bi;
+    sk[warp] = bk;
   }
   __syncthreads();
   if (warp == 0) {
     bs = ss[lane];
     bi = si[lane];
+    bk = sk[lane];
     for (int o = 16; o > 0; o >>= 1) {
       const double os = __shfl_down_sync(0xffffffffu, bs, o);
       const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+      const unsigned ok = __shfl_down_sync(0xffffffffu, bk, o);
       if (loop_better(os, oi, bs, bi)) {
         bs = os;
         bi = oi;
+        bk = ok;
       }
     }
     if (lane == 0) {
       ss[0] = bs;
       si[0] = bi;
+      sk[0] = bk;
     }
   }
   __syncthreads();
   bi = si[0];
   bs = ss[0];
+  bk = sk[0];
   if (bi < 0) {  // no feasible assignment left (reduce.cpp:404)
     if (tid == 0) st->done = 1;
     return;
   }
   const int it = st->iter;
-  const int s = a.cs[bi], r = a.cr[bi];
+  const int s = int(bk >> 16), r = int(bk & 0xffffu);
   const int L = a.L;
   if (it < a.cap) {
     if (tid == 0) {
@@ -606,11 +623,11 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
     }
   }
   for (int j = tid; j < a.n; j += kLoopThreads)
-    if (a.sup[j] == r) a.sup[j] = s;
+    if ((j == tid ? sup0 : a.sup[j]) == r) a.sup[j] = s;
   // remove r from the ascending active list
   const int ns = st->ns;
   for (int k = tid; k < ns; k += kLoopThreads)
-    if (a.sn[k] == r) s_pos = k;
+    if ((k == tid ? sn0 : a.sn[k]) == r) s_pos = k;
   __syncthreads();
   // shift the tail left by one, a block-wide chunk at a time (each chunk is
   // read completely before any of it is written)
