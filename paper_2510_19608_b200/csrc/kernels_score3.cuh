@@ -70,6 +70,12 @@ struct S3Layout {
 #ifndef S3_NNMAX
 #define S3_NNMAX 1
 #endif
+#ifndef S3_MIN_BLOCKS  // tuning: resident CTAs the register budget is sized for
+#define S3_MIN_BLOCKS 3
+#endif
+#ifndef S3_NRT1  // tuning: rows per straight-line pass for single-phase candidates
+#define S3_NRT1 4
+#endif
 #ifndef S3_HH_UNROLL
 #define S3_HH_UNROLL 0
 #endif
@@ -488,7 +494,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     // this warp's candidates: straight-line passes with the all-first fold;
     // any other tile: the same fast passes with per-row fixups and a
     // flag-driven fold
-    constexpr int NRT = NL == 1 ? 8 : 4;  // rows per pass (register budget)
+    constexpr int NRT = NL == 1 ? S3_NRT1 : 4;  // rows per pass (register budget)
     if (tflag && !__any_sync(0xffffffffu, j == (ts0 >> 4) || j == (tr0 >> 4))) {
 #if S3_HH_UNROLL
 #pragma unroll
@@ -559,7 +565,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   }
 }
 
-__global__ void __launch_bounds__(128, 3) score3_kernel(S3Args a) {
+__global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
   extern __shared__ double sm_dyn[];
   const int b = blockIdx.x;
   griddep_wait();
