@@ -190,16 +190,24 @@ struct Engine::Impl {
   DBuf<double2> merr_yin, merr_rhs, merr_out, merr_kv;
   DBuf<int> d_grpdone;  // score3 slice-completion counters
   // score3 geometry: 16 Z-column slots per CTA, scenario slices of up to 8
-  static constexpr int kS3Slots = 16;
-  int s3_ls() const { return std::min(L, 8); }
+  // scorer geometry: Z-column slots per CTA and scenario-slice width
+  // (KRONRED_S3_G / KRONRED_S3_LS: tuning overrides, slots x width <= 128)
+  // (with one or two scenarios a CTA is a single warp: twice the slots keep
+  // two warps per CTA; 8,381 nodes x 2 scenarios 10.0 -> 9.0 s)
+  int s3_slots() const {
+    if (const char* e = std::getenv("KRONRED_S3_G")) return std::atoi(e);
+    return L <= 2 ? 32 : 16;
+  }
+  const int kS3Ls = std::getenv("KRONRED_S3_LS") ? std::atoi(std::getenv("KRONRED_S3_LS")) : 8;
+  int s3_ls() const { return std::min(L, kS3Ls); }
   int s3_ldc() const { return std::max(2 * n, 2 * int(prob.net.branches.size()) + 1); }
   int s3_nsl() const { return (L + s3_ls() - 1) / s3_ls(); }
-  int s3_threads() const { return (kS3Slots * s3_ls() + 31) / 32 * 32; }
+  int s3_threads() const { return (s3_slots() * s3_ls() + 31) / 32 * 32; }
   S3Args s3_args() const {
     S3Args q{};
     q.L = L;
     q.nphi = nphi;
-    q.G = kS3Slots;
+    q.G = s3_slots();
     q.Ls = s3_ls();
     q.nsl = s3_nsl();
     q.cand = d_cand.p;
@@ -256,6 +264,9 @@ struct Engine::Impl {
   double loop_key_ebar = -1.0, loop_key_target = -1.0;
   int loop_key_has = -1;
   bool loop_key_trace = false;
+  // buffers the captured graph refers to (a reload may reallocate them)
+  const void* loop_key_bufs[4] = {nullptr, nullptr, nullptr, nullptr};
+  int loop_key_L = -1;
   DBuf<unsigned long long> d_tdbg;
   bool loop_trace = std::getenv("KRONRED_LOOP_TRACE") != nullptr;
   bool force_host_loop = std::getenv("KRONRED_LOOP") != nullptr && std::string(std::getenv("KRONRED_LOOP")) == "host";
@@ -1210,11 +1221,11 @@ struct Engine::Impl {
       for (int k = 1; k <= 3; ++k) {
         q.grp_start[k] = grp_off[k - 1];
         q.grp_cta[k - 1] = c3;
-        c3 += (grp_off[k] - grp_off[k - 1] + kS3Slots / k - 1) / (kS3Slots / k) * q.nsl;
+        c3 += (grp_off[k] - grp_off[k - 1] + s3_slots() / k - 1) / (s3_slots() / k) * q.nsl;
       }
       q.grp_cta[3] = c3;
       if (c3 > 0) {
-        score3_kernel<<<c3, s3_threads(), S3Layout{s3_ls(), kS3Slots}.smem_bytes(), stream>>>(q);
+        score3_kernel<<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
         launched();
         CK(cudaGetLastError());
       }
@@ -1349,7 +1360,7 @@ struct Engine::Impl {
     a.kcap = int(enum_kcap());
     a.inc_enum = std::getenv("KRONRED_ENUM_FULL") == nullptr ? 1 : 0;
     a.nsl = s3_nsl();
-    for (int k = 1; k <= 3; ++k) a.cpc[k] = kS3Slots / k;
+    for (int k = 1; k <= 3; ++k) a.cpc[k] = s3_slots() / k;
     a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
     a.has_target = cfg.target_reduction ? 1 : 0;
     a.target = cfg.target_reduction ? *cfg.target_reduction : 0.0;
@@ -1466,8 +1477,10 @@ struct Engine::Impl {
     enum_kernel<<<1, kLoopThreads, enum_smem(), stream>>>(la);
     launched();
     CK(cudaGetLastError());
+    const void* bufs[4] = {d_bv.p, d_iagg.p, d_pmaxerr.p, d_tfwd.p};
     const bool key_ok = loop_exec && loop_key_ebar == cfg.e_bar && loop_key_has == la.has_target &&
-                        loop_key_target == la.target && loop_key_trace == loop_trace;
+                        loop_key_target == la.target && loop_key_trace == loop_trace && loop_key_L == L &&
+                        std::equal(bufs, bufs + 4, loop_key_bufs);
     if (!key_ok) {
       if (loop_exec) CK(cudaGraphExecDestroy(loop_exec));
       if (loop_graph) CK(cudaGraphDestroy(loop_graph));
@@ -1497,7 +1510,7 @@ struct Engine::Impl {
       q.st = d_loopst.p;
       q.tdbg = la.tdbg;
       int occ = 0;
-      const size_t sm3 = S3Layout{s3_ls(), kS3Slots}.smem_bytes();
+      const size_t sm3 = S3Layout{s3_ls(), s3_slots()}.smem_bytes();
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score3_kernel, s3_threads(), sm3));
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -1527,6 +1540,8 @@ struct Engine::Impl {
       loop_key_has = la.has_target;
       loop_key_target = la.target;
       loop_key_trace = loop_trace;
+      loop_key_L = L;
+      std::copy(bufs, bufs + 4, loop_key_bufs);
     }
     // the whole loop: one graph launch (a loop that is already done runs one
     // body of early-exit kernels); results come back with one sync
