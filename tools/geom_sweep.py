@@ -1,0 +1,32 @@
+"""Tuning aid: scorer geometry sweep (Z-column slots per CTA x scenario-slice
+width, the KRONRED_S3_G / KRONRED_S3_LS overrides) on a golden case.
+`python tools/geom_sweep.py [case] [target] [G:Ls ...]`; prints one JSON line
+per geometry with the best device time of three full reductions."""
+import json, os, sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+import paper_2510_19608_b200 as kr  # noqa: E402
+from golden_io import path  # noqa: E402
+
+args = [a for a in sys.argv[1:] if ":" not in a]
+case = args[0] if args else "c2"
+target = float(args[1]) if len(args) > 1 else None
+geoms = [a for a in sys.argv[1:] if ":" in a] or ["16:8", "8:8", "16:4", "32:4", "8:16", "24:4", "12:8"]
+hp = kr.HostProblem(str(path(case, "net.json")), str(path(case, "scen.csv")))
+ref = None
+for g in geoms:
+    G, Ls = g.split(":")
+    os.environ["KRONRED_S3_G"], os.environ["KRONRED_S3_LS"] = G, Ls
+    ctx = kr.Context(hp, device=0)
+    cfg = kr.ReductionConfig(e_bar=3e-3, target_reduction=target)
+    ms, sig = [], None
+    for _ in range(3):
+        r = ctx.run_reduction(cfg)
+        ms.append(r.device_ms)
+        sig = [(t.s, t.r, t.smice) for t in r.trace]
+    ref = sig if ref is None else ref
+    print(json.dumps({"case": case, "G": int(G), "Ls": int(Ls), "iterations": len(r.trace),
+                      "best_ms": min(ms), "same_decisions": sig == ref}), flush=True)
+    del ctx
