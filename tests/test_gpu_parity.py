@@ -269,3 +269,17 @@ def test_c4_96_scenarios_first_iterations_bitwise(tmp_path):
     ctx = kr.Context(kr.HostProblem(str(path("c4", "net.json")), str(scen)))
     res = ctx.run_reduction(cfg_from_flags([f for f in meta["flags"] if f not in ("--workers", "0")]))
     assert_trace(res, "c4L96", tag)
+
+
+@pytest.mark.parametrize("G,Ls", [(8, 8), (16, 4), (12, 8), (8, 16), (32, 2)])
+def test_scorer_geometry_overrides_bitwise(G, Ls, monkeypatch):
+    """Scorer geometry (Z-column slots per CTA x scenario-slice width, the
+    KRONRED_S3_G / KRONRED_S3_LS tuning overrides; tools/geom_sweep.py) changes
+    only how (candidate, scenario) pairs are tiled, never the per-pair
+    arithmetic or the scenario-order sum: the reference trace is reproduced
+    bit for bit, including a ragged last slice (8 x 16 at L = 24) and a slot
+    count that is not a power of two (12)."""
+    monkeypatch.setenv("KRONRED_S3_G", str(G))
+    monkeypatch.setenv("KRONRED_S3_LS", str(Ls))
+    res = kr.Context(host("c2")).run_reduction(kr.ReductionConfig(e_bar=3e-3))
+    assert_trace(res, "c2", "mag_3e-3")
