@@ -174,7 +174,7 @@ struct AssignmentState {
   std::vector<std::vector<int>> members;
   std::vector<int> supernodes;
   std::vector<std::vector<int>> lambda;
-  std::vector<std::vector<cx>> i_agg;  // host mirror is not maintained (device-resident)
+  std::vector<std::vector<cx>> i_agg;  // per scenario, 3n aggregated injections (reduce.hpp:53)
   int supernode_count() const { return int(supernodes.size()); }
   double reduction_fraction() const {
     return n == 0 ? 0.0 : double(n - supernode_count()) / double(n);

@@ -148,9 +148,20 @@ int cmd_reduce(const std::map<std::string, std::string>& a) {
   const ScenarioLibrary lib = load_library(net, gets(a, "scen", ""));
   const ReductionConfig cfg = make_cfg(a);
   long long cands = 0;
+  // --trace-hex rows are streamed from the observer (one flushed line per
+  // commit, reduce.cpp:423) so a long golden run leaves a usable prefix even
+  // if it is stopped; the `final` line is appended after the run.
+  std::ofstream hexout;
+  if (a.count("trace-hex")) hexout.open(gets(a, "trace-hex", ""));
   const auto t0 = std::chrono::steady_clock::now();
   ReductionResult res = run_reduction(net, lib, cfg, [&](const AssignmentState&, const TraceRow& r) {
     cands += r.candidate_count;
+    if (hexout.is_open()) {
+      hexout << r.iteration << " " << r.s << " " << r.r << " " << hx(r.smice);
+      for (double e : r.max_err) hexout << " " << hx(e);
+      hexout << " " << r.supernode_count << " " << r.candidate_count << "\n";
+      hexout.flush();
+    }
   });
   const auto t1 = std::chrono::steady_clock::now();
   ReducedModel model = std::move(res.model);
@@ -166,16 +177,10 @@ int cmd_reduce(const std::map<std::string, std::string>& a) {
     for (TraceRow& r : tr) r.wall_ms = 0;
     write_trace_csv(gets(a, "trace", ""), tr, model.scenario_ids, model.final_max_err);
   }
-  if (a.count("trace-hex")) {
-    std::ofstream out(gets(a, "trace-hex", ""));
-    for (const TraceRow& r : res.trace) {
-      out << r.iteration << " " << r.s << " " << r.r << " " << hx(r.smice);
-      for (double e : r.max_err) out << " " << hx(e);
-      out << " " << r.supernode_count << " " << r.candidate_count << "\n";
-    }
-    out << "final";
-    for (double e : model.final_max_err) out << " " << hx(e);
-    out << "\n";
+  if (hexout.is_open()) {
+    hexout << "final";
+    for (double e : model.final_max_err) hexout << " " << hx(e);
+    hexout << "\n";
   }
   std::printf(
       "{\"wall_s\": %.6f, \"iterations\": %zu, \"candidates\": %lld, \"cand_per_s\": %.3f, "

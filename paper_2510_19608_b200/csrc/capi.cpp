@@ -333,17 +333,6 @@ ReductionConfig cfg_from_c(const krg_config* c) {
   return cfg;
 }
 
-AssignmentState to_public(const HostState& hs) {
-  AssignmentState st;
-  st.n = hs.n;
-  st.slack = hs.slack;
-  st.sup = hs.sup;
-  st.members = hs.members;
-  st.supernodes = hs.supernodes;
-  st.lambda = hs.lambda;
-  return st;
-}
-
 int device_from_env() {
   if (const char* e = std::getenv("KRONRED_DEVICE")) return std::atoi(e);
   return -1;  // current device of the calling thread
@@ -387,12 +376,12 @@ ReductionResult run_reduction(const Network& net, const ScenarioLibrary& lib, co
   Engine eng(problem_from(net, &lib), device_from_env());
   ResultData rd;
   Engine::Observer obs;
-  if (observer) obs = [&](const HostState& hs, const TraceRow& row) { observer(to_public(hs), row); };
+  if (observer) obs = [&](const HostState& hs, const TraceRow& row) { observer(hs, row); };
   eng.run(cfg, obs, rd);
   ReductionResult res;
   res.model = std::move(rd.model);
   res.trace = std::move(rd.trace);
-  res.state = to_public(rd.state);
+  res.state = static_cast<AssignmentState&&>(std::move(rd.state));
   return res;
 }
 

@@ -265,7 +265,8 @@ struct Engine::Impl {
   int loop_key_has = -1;
   bool loop_key_trace = false;
   // buffers the captured graph refers to (a reload may reallocate them)
-  const void* loop_key_bufs[4] = {nullptr, nullptr, nullptr, nullptr};
+  static constexpr int kLoopKeyBufs = 18;
+  const void* loop_key_bufs[kLoopKeyBufs] = {};
   int loop_key_L = -1;
   DBuf<unsigned long long> d_tdbg;
   bool loop_trace = std::getenv("KRONRED_LOOP_TRACE") != nullptr;
@@ -955,6 +956,10 @@ struct Engine::Impl {
     d_v0.alloc(size_t(3) * n);
     d_v0p.alloc(size_t(std::max(nphi, 1)));
     d_cand.alloc(size_t(2 * n));
+    // candidate lists: sized once for both the host-fed (2n) and the device
+    // loop (2 nb + 1) paths, never reallocated (the loop graph captures them)
+    d_cs.alloc(size_t(2 * std::max(n, int(prob.net.branches.size()))) + 1);
+    d_cr.alloc(size_t(2 * std::max(n, int(prob.net.branches.size()))) + 1);
     d_snt.alloc(size_t(n));
     d_snid.alloc(size_t(n));
     d_memoff.alloc(size_t(n) + 1);
@@ -1059,7 +1064,7 @@ struct Engine::Impl {
     CK(cudaGetLastError());
     build_z();
     refresh_base();
-    hs.init(prob.net);
+    hs.init(prob.net, &prob.injections, L);
     loop_active = true;
   }
 
@@ -1070,8 +1075,6 @@ struct Engine::Impl {
     const long long C = c1 - c0;
     if (!cfg.use_delta) {
       // full-solve path: candidate lists + super-node / member CSR
-      d_cs.alloc(size_t(2 * n) + 1);
-      d_cr.alloc(size_t(2 * n) + 1);
       if (C > 0) {
         CK(cudaMemcpyAsync(d_cs.p, cs.data() + c0, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
         CK(cudaMemcpyAsync(d_cr.p, cr.data() + c0, size_t(C) * sizeof(int), cudaMemcpyHostToDevice, stream));
@@ -1422,8 +1425,6 @@ struct Engine::Impl {
     d_sup.alloc(size_t(n));
     d_sn.alloc(size_t(n));
     d_tabnode.alloc(size_t(n));
-    d_cs.alloc(size_t(2 * nb) + 1);
-    d_cr.alloc(size_t(2 * nb) + 1);
     d_brf.alloc(size_t(nb) + 1);
     d_brt.alloc(size_t(nb) + 1);
     d_trsr.alloc(size_t(2 * n));
@@ -1477,10 +1478,12 @@ struct Engine::Impl {
     enum_kernel<<<1, kLoopThreads, enum_smem(), stream>>>(la);
     launched();
     CK(cudaGetLastError());
-    const void* bufs[4] = {d_bv.p, d_iagg.p, d_pmaxerr.p, d_tfwd.p};
+    const void* bufs[kLoopKeyBufs] = {d_bv.p,   d_iagg.p, d_pmaxerr.p, d_tfwd.p,   d_cs.p,   d_cr.p,
+                                      d_cand.p, d_cidx.p, d_pcand.p,   d_iaggp.p,  d_tab.p,  d_tplain.p,
+                                      d_Z.p,    d_psmice.p, d_grpdone.p, d_loopst.p, d_trme.p, d_sup.p};
     const bool key_ok = loop_exec && loop_key_ebar == cfg.e_bar && loop_key_has == la.has_target &&
                         loop_key_target == la.target && loop_key_trace == loop_trace && loop_key_L == L &&
-                        std::equal(bufs, bufs + 4, loop_key_bufs);
+                        std::equal(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     if (!key_ok) {
       if (loop_exec) CK(cudaGraphExecDestroy(loop_exec));
       if (loop_graph) CK(cudaGraphDestroy(loop_graph));
@@ -1541,14 +1544,17 @@ struct Engine::Impl {
       loop_key_target = la.target;
       loop_key_trace = loop_trace;
       loop_key_L = L;
-      std::copy(bufs, bufs + 4, loop_key_bufs);
+      std::copy(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     }
     // the whole loop: one graph launch (a loop that is already done runs one
     // body of early-exit kernels); results come back with one sync
     CK(cudaGraphLaunch(loop_exec, stream));
-    if (!h_loopst) {
-      CK(cudaMallocHost(&h_loopst, sizeof(LoopState)));
+    if (!h_loopst) CK(cudaMallocHost(&h_loopst, sizeof(LoopState)));
+    if (!h_trace || h_trace_cap < trace_bytes()) {  // a reload may bring more scenarios
+      if (h_trace) CK(cudaFreeHost(h_trace));
+      h_trace = nullptr;
       CK(cudaMallocHost(&h_trace, trace_bytes()));
+      h_trace_cap = trace_bytes();
     }
     CK(cudaMemcpyAsync(h_loopst, d_loopst.p, sizeof(LoopState), cudaMemcpyDeviceToHost, stream));
     {
@@ -1561,7 +1567,7 @@ struct Engine::Impl {
       p += sizeof(double) * size_t(n);
       CK(cudaMemcpyAsync(p, d_trme.p, sizeof(double) * size_t(n) * L, cudaMemcpyDeviceToHost, stream));
       p += sizeof(double) * size_t(n) * L;
-      CK(cudaMemcpyAsync(p, d_trt.p, sizeof(unsigned long long) * size_t(n), cudaMemcpyDeviceToHost, stream));
+      CK(cudaMemcpyAsync(p, d_trt.p, sizeof(unsigned long long) * (size_t(n) + 1), cudaMemcpyDeviceToHost, stream));
     }
     CK(cudaStreamSynchronize(stream));
     check_deferred_fail();
@@ -1621,16 +1627,18 @@ struct Engine::Impl {
       for (int i = 0; i < it; ++i) {
         tr_s[size_t(i)] = sr[2 * i];
         tr_r[size_t(i)] = sr[2 * i + 1];
-        if (i > 0) tr_ms[size_t(i)] = double(tt[i] - tt[i - 1]) * 1e-6;
+        tr_ms[size_t(i)] = double(tt[i] - (i > 0 ? tt[i - 1] : tt[n])) * 1e-6;
       }
     }
   }
 
   size_t trace_bytes() const {
-    return size_t(n) * (sizeof(int) * 3 + sizeof(double) * (1 + size_t(L)) + sizeof(unsigned long long));
+    return size_t(n) * (sizeof(int) * 3 + sizeof(double) * (1 + size_t(L))) +
+           (size_t(n) + 1) * sizeof(unsigned long long);
   }
   LoopState* h_loopst = nullptr;
   char* h_trace = nullptr;
+  size_t h_trace_cap = 0;
 
   void commit_device(int s, int r) {
     const unsigned ms = prob.mask[size_t(s)], mr = prob.mask[size_t(r)];

@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   }
   const int ns = st->ns;
   if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 2] = globaltimer();
+  if (st->iter == 0 && tid == 0) a.tr_t[a.cap] = globaltimer();  // loop start: iteration 1's wall_ms
 #ifdef ENUM_TIMING
   long long et[9];
 #endif

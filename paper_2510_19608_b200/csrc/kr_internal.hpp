@@ -76,20 +76,14 @@ ElimSchedule build_schedule(const FlatBlocks& y, const std::vector<std::uint8_t>
                             const std::vector<int>& elim_set);
 
 // ---------------------------------------------------------------------------
-// Host assignment state machine (reduce.cpp:39-73, 299-344), integer part.
-struct HostState {
-  int n = 0, slack = -1;
-  std::vector<int> sup;
-  std::vector<std::vector<int>> members;
-  std::vector<int> supernodes;                // ascending
-  std::vector<std::vector<int>> lambda;       // sorted
+// Host assignment state machine (reduce.cpp:39-73, 299-344): the public
+// AssignmentState (so observers receive it without a copy) plus phase masks.
+struct HostState : AssignmentState {
   std::vector<std::uint8_t> mask;
-  void init(const Network& net);
+  // injections: [L][3n][2] scenario currents (the i_agg mirror), or null
+  void init(const Network& net, const std::vector<double>* injections = nullptr, int scenarios = 0);
   void enumerate(std::vector<int>& cs, std::vector<int>& cr) const;
   void commit(int s, int r);
-  double reduction_fraction() const {
-    return n == 0 ? 0.0 : double(n - int(supernodes.size())) / double(n);
-  }
 };
 
 // ---------------------------------------------------------------------------

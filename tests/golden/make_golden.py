@@ -96,6 +96,83 @@ def large() -> None:
             gz(d / f)
 
 
+def _inflate(case: str, name: str) -> Path:
+    """Plain copy of a gzipped fixture input (the reference reads plain files)."""
+    import gzip as _gz
+    import tempfile
+    src = HERE / case / (name + ".gz")
+    dst = Path(tempfile.gettempdir()) / "kronred_long" / case / name
+    dst.parent.mkdir(parents=True, exist_ok=True)
+    with _gz.open(src, "rb") as f, open(dst, "wb") as g:
+        shutil.copyfileobj(f, g)
+    return dst
+
+
+def _reduce_files(case: str, tag: str, net: Path, scen: Path, *flags: str, reduced: bool) -> dict:
+    d = HERE / case
+    d.mkdir(exist_ok=True)
+    args = ["reduce", "--net", str(net), "--scen", str(scen), "--trace-hex", str(d / f"trace_{tag}.txt"),
+            *flags]
+    if reduced:
+        args += ["--reduced", str(d / f"reduced_{tag}.json")]
+    out = json.loads(run(*args))
+    meta = d / "runs.json"
+    runs = json.loads(meta.read_text()) if meta.exists() else {}
+    runs[tag] = {"flags": list(flags), "radialize": False, "iterations": out["iterations"],
+                 "candidates": out["candidates"], "kept": out["kept"], "ref_wall_s": out["wall_s"],
+                 "ref_workers": out["workers"]}
+    meta.write_text(json.dumps(runs, indent=1, sort_keys=True) + "\n")
+    gz(d / f"trace_{tag}.txt")
+    if reduced:
+        gz(d / f"reduced_{tag}.json")
+    return out
+
+
+def long(which: list[str]) -> None:
+    """Whole-run / long-prefix goldens for BASELINE configs[2..4] (VERDICT r1
+    item 1). Each step is independent; run in the background (hours of CPU):
+
+      h2k   2,000-node three-phase-heavy feeder (frac2=0.003, frac1=0.005),
+            5 scenarios, e_bar 3e-3, full run + first-2-iteration scores
+      c3    5,991 nodes, 2 scenarios, e_bar 3e-3, target 0.9 (full run)
+      c4L24 8,381 nodes, 24 scenarios, first 200 iterations
+      c5    8,381 nodes, 96 scenarios, e_bar 1e-3, first 50 iterations
+      c4    8,381 nodes, 2 scenarios, e_bar 3e-3, target 0.8 (full run)
+
+    c4L24 / c5 libraries are too large to commit; the GPU tests regenerate
+    them with the reference generator in oracle/_ref (params.json)."""
+    import tempfile
+    tmp = Path(tempfile.gettempdir()) / "kronred_long"
+    tmp.mkdir(exist_ok=True)
+    for w in which:
+        if w == "h2k":
+            d = gen("h2k", n=2000, seed=2000, L=5, branching=0.3, frac2=0.003, frac1=0.005)
+            reduce(d, "mag_3e-3", "--e-bar", "3e-3", "--workers", "0")
+            scores(d, "mag_3e-3", 2, "--e-bar", "3e-3")
+            for f in ["net.json", "scen.csv", "trace_mag_3e-3.txt", "reduced_mag_3e-3.json", "scores_mag_3e-3.txt"]:
+                gz(d / f)
+        elif w == "c3":
+            _reduce_files("c3", "mag_3e-3_t09", _inflate("c3", "net.json"), _inflate("c3", "scen.csv"),
+                          "--e-bar", "3e-3", "--target", "0.9", "--workers", "0", reduced=True)
+        elif w == "c4":
+            _reduce_files("c4", "mag_3e-3_t08", _inflate("c4", "net.json"), _inflate("c4", "scen.csv"),
+                          "--e-bar", "3e-3", "--target", "0.8", "--workers", "0", reduced=True)
+        elif w in ("c4L24", "c5"):
+            L, e, k = (24, "3e-3", 200) if w == "c4L24" else (96, "1e-3", 50)
+            d = HERE / w
+            d.mkdir(exist_ok=True)
+            params = {"n": 8381, "seed": 8381, "L": L, "branching": 0.3}
+            (d / "params.json").write_text(json.dumps(params, indent=1) + "\n")
+            net, scen = tmp / f"{w}_net.json", tmp / f"{w}_scen.csv"
+            run("gen", "--n", "8381", "--seed", "8381", "--L", str(L), "--branching", "0.3",
+                "--net", str(net), "--scen", str(scen))
+            assert net.read_bytes() == _inflate("c4", "net.json").read_bytes()
+            _reduce_files(w, f"mag_{e}_k{k}", net, scen, "--e-bar", e, "--target", repr(k / 8381 + 1e-12),
+                          "--workers", "0", reduced=False)
+        else:
+            raise SystemExit(f"unknown long step {w}")
+
+
 def naive() -> None:
     """use_delta = false (eval_full_solve, reduce.cpp:132-167) on the small
     feeders: its full solves round differently from the delta path."""
@@ -110,6 +187,9 @@ def main() -> None:
         sys.exit("build oracle/_ref first: make -C oracle")
     if sys.argv[1:] == ["large"]:
         large()
+        return
+    if sys.argv[1:2] == ["long"]:
+        long(sys.argv[2:] or ["h2k", "c3", "c4L24", "c5", "c4"])
         return
     if sys.argv[1:] == ["naive"]:
         naive()
