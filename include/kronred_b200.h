@@ -151,7 +151,9 @@ int krg_set_exchange(krg_ctx* ctx, int32_t rank, int32_t world, krg_exchange_fn 
 /* Number of kernels this context has launched so far. */
 int64_t krg_launch_count(const krg_ctx* ctx);
 /* Per-kernel CUDA-event timing on the launching stream (bench/roofline only):
- * which = 0 score kernel, 1 base-refresh solve. Sums over launches of the
+ * which = 0 scorer (score1_kernel: |phi(r)| = 1 candidates, the dominant
+ * kernel), 1 base-refresh solve, 2 score3_kernel (|phi(r)| >= 2 candidates
+ * next to score1). Sums over launches of the
  * event time and of the algorithmic flops/bytes. */
 int krg_set_profile(krg_ctx* ctx, int32_t on);
 int krg_kernel_stats(const krg_ctx* ctx, int32_t which, int64_t* launches, double* ms,

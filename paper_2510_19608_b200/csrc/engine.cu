@@ -75,6 +75,7 @@ struct DBuf {
 #include "kernels_csolve.cuh"
 #include "kernels_score.cuh"
 #include "kernels_score3.cuh"
+#include "kernels_score1.cuh"
 #include "kernels_loop.cuh"
 #include "kernels_naive.cuh"
 
@@ -195,19 +196,46 @@ struct Engine::Impl {
   // (with one or two scenarios a CTA is a single warp: twice the slots keep
   // two warps per CTA; 8,381 nodes x 2 scenarios 10.0 -> 9.0 s)
   int s3_slots() const {
-    if (const char* e = std::getenv("KRONRED_S3_G")) return std::atoi(e);
+    if (const char* e = std::getenv("KRONRED_S3_G")) {
+      const int g = std::atoi(e);
+      if (g < 3 || g > 128) throw ConfigError("KRONRED_S3_G must lie in [3, 128]");
+      return g;
+    }
     return L <= 2 ? 32 : 16;
+  }
+  // row split (lanes per pair): KRONRED_S3_S forces 1/2/4; otherwise the widest
+  // split that keeps pairs x lanes within KRONRED_S3_FILL threads (default one
+  // wave of 3 resident 128-thread CTAs on every SM)
+  const int s3_force = std::getenv("KRONRED_S3_S") ? std::atoi(std::getenv("KRONRED_S3_S")) : 0;
+  long long s3_fill() const {
+    if (const char* e = std::getenv("KRONRED_S3_FILL")) return std::atoll(e);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return (long long)sms * 3 * 128;
+  }
+  // slice-completion counters: one per candidate group at the widest split
+  size_t s3_groups_max() const {
+    size_t g = 8;
+    for (int k = 1; k <= 3; ++k) g += size_t(s3_ldc() + s3_cpc(s3_slots(), k, 4) - 1) / size_t(s3_cpc(s3_slots(), k, 4));
+    return g;
   }
   const int kS3Ls = std::getenv("KRONRED_S3_LS") ? std::atoi(std::getenv("KRONRED_S3_LS")) : 8;
   int s3_ls() const { return std::min(L, kS3Ls); }
   int s3_ldc() const { return std::max(2 * n, 2 * int(prob.net.branches.size()) + 1); }
   int s3_nsl() const { return (L + s3_ls() - 1) / s3_ls(); }
-  int s3_threads() const { return (s3_slots() * s3_ls() + 31) / 32 * 32; }
+  int s3_threads() const {
+    const int t = (s3_slots() * s3_ls() + 31) / 32 * 32;
+    if (t > 128) throw ConfigError("scorer geometry: slots x slice width must not exceed 128 threads");
+    return t;
+  }
   S3Args s3_args() const {
     S3Args q{};
     q.L = L;
     q.nphi = nphi;
     q.G = s3_slots();
+    q.S = 1;
+    q.ns_max = std::getenv("KRONRED_S3_NS") ? std::max(3, std::atoi(std::getenv("KRONRED_S3_NS"))) : 8;
+    q.s_multi = s3_multi_lanes();
     q.Ls = s3_ls();
     q.nsl = s3_nsl();
     q.cand = d_cand.p;
@@ -226,6 +254,64 @@ struct Engine::Impl {
     q.grp_done = d_grpdone.p;
     q.tplain = d_tplain.p;
     return q;
+  }
+
+  // score1 (kernels_score1.cuh) takes the |phi(r)| = 1 candidates when the
+  // scorer runs its default geometry (16 slots, slices of 8 scenarios)
+  bool s1_ok() const {
+    return s3_ls() == kS1Ls && s3_slots() == kS1G && L <= 128 && std::getenv("KRONRED_NO_S1") == nullptr;
+  }
+  // candidates per score1 item at S = 1, 2, 4 (KRONRED_S1_GK="8,8,4" tuning;
+  // supported: 16/8 at S = 1 and 2, 8/4 at S = 4)
+  int s1_gk[3] = {8, 8, 4};
+  void parse_s1_gk() {
+    if (const char* e = std::getenv("KRONRED_S1_GK")) {
+      int a = 16, b = 8, c = 4;
+      if (std::sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && (a == 16 || a == 8) && (b == 16 || b == 8) && (c == 8 || c == 4)) {
+        s1_gk[0] = a;
+        s1_gk[1] = b;
+        s1_gk[2] = c;
+      } else {
+        throw ConfigError("KRONRED_S1_GK: three of 16|8, 16|8, 8|4");
+      }
+    }
+  }
+  template <int S, int GK>
+  void launch_s1_k(const S3Args& q, int grid, cudaStream_t st) {
+    score1_kernel<S, GK><<<grid, S1Geom<S, GK>::P, s1_smem_bytes<S, GK>(), st>>>(q);
+  }
+  void launch_s1(int S, const S3Args& q, int grid, cudaStream_t st) {
+    if (grid <= 0) return;
+    const int gk = s1_gk[s1_switch_index(S)];
+    if (S == 1)
+      gk == 16 ? launch_s1_k<1, 16>(q, grid, st) : launch_s1_k<1, 8>(q, grid, st);
+    else if (S == 2)
+      gk == 16 ? launch_s1_k<2, 16>(q, grid, st) : launch_s1_k<2, 8>(q, grid, st);
+    else
+      gk == 8 ? launch_s1_k<4, 8>(q, grid, st) : launch_s1_k<4, 4>(q, grid, st);
+    launched();
+    CK(cudaGetLastError());
+  }
+  // occupancy-sized persistent grid of the score1 variant for split S
+  int s1_grid(int S, int items_max) {
+    const int gk = s1_gk[s1_switch_index(S)];
+    int occ = 0;
+    auto occ_of = [&](auto kern, int P, size_t sm) { CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P, sm)); };
+    if (S == 1)
+      gk == 16 ? occ_of(score1_kernel<1, 16>, 128, s1_smem_bytes<1, 16>()) : occ_of(score1_kernel<1, 8>, 64, s1_smem_bytes<1, 8>());
+    else if (S == 2)
+      gk == 16 ? occ_of(score1_kernel<2, 16>, 256, s1_smem_bytes<2, 16>()) : occ_of(score1_kernel<2, 8>, 128, s1_smem_bytes<2, 8>());
+    else
+      gk == 8 ? occ_of(score1_kernel<4, 8>, 256, s1_smem_bytes<4, 8>()) : occ_of(score1_kernel<4, 4>, 128, s1_smem_bytes<4, 4>());
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    return std::max(1, std::min(items_max * 2, std::max(1, occ) * sms));
+  }
+  static int s1_switch_index(int S) { return S == 1 ? 0 : (S == 2 ? 1 : 2); }
+  // split of the |phi(r)| >= 2 candidates next to score1 (KRONRED_S3_MULTI)
+  int s3_multi_lanes() const {
+    const int v = std::getenv("KRONRED_S3_MULTI") ? std::atoi(std::getenv("KRONRED_S3_MULTI")) : 4;
+    return (v == 1 || v == 2 || v == 4) ? v : 4;
   }
 
   // threads per scorer CTA: a multiple of L (whole candidates) and of 32
@@ -249,15 +335,49 @@ struct Engine::Impl {
   // kernel statistics (enabled on demand; CUDA events on the launching stream)
   bool profile = false;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_run0 = nullptr, ev_run1 = nullptr;
-  KernelStats score_stats{}, solve_stats{};
+  KernelStats score_stats{}, solve_stats{}, multi_stats{};
   long long score_c0 = 0;
   // device-resident loop (kernels_loop.cuh)
   DBuf<LoopState> d_loopst;
   DBuf<int> d_sup, d_sn, d_tabnode, d_cs, d_cr, d_brf, d_brt, d_trsr, d_trc;
   DBuf<double> d_trsmice, d_trme;
   DBuf<unsigned long long> d_trt;
-  cudaStream_t stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t stream2 = nullptr, stream3 = nullptr, stream_cap = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork3 = nullptr, ev_join3 = nullptr;
+  // Inside a stream capture: a switch conditional node on `h` with three
+  // bodies; body i is captured by launch(i, capture stream).
+  template <class F>
+  void add_switch(cudaStream_t st, cudaGraphConditionalHandle h, F&& launch) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    const cudaGraphEdgeData* ed = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo_v3(st, &cs, nullptr, &g, &deps, &ed, &nd));
+    if (cs != cudaStreamCaptureStatusActive) throw Error("add_switch outside a capture");
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeSwitch;
+    cp.conditional.size = 3;
+    cudaGraphNode_t node;
+    {
+      const cudaError_t e = cudaGraphAddNode_v2(&node, g, deps, ed, nd, &cp);
+      if (e != cudaSuccess) {
+        std::string why = "add_switch: cudaGraphAddNode (" + std::to_string(nd) + " deps";
+        for (size_t i = 0; ed && i < nd; ++i) why += ", edge type " + std::to_string(int(ed[i].type)) + " port " + std::to_string(int(ed[i].from_port));
+        throw CudaError(why + "): " + cudaGetErrorString(e));
+      }
+    }
+    if (!stream_cap) CK(cudaStreamCreateWithFlags(&stream_cap, cudaStreamNonBlocking));
+    for (int i = 0; i < 3; ++i) {
+      cudaGraph_t bg = cp.conditional.phGraph_out[i];
+      CK(cudaStreamBeginCaptureToGraph(stream_cap, bg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      launch(i, stream_cap);
+      CK(cudaStreamEndCapture(stream_cap, &bg));
+    }
+    CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  }
   // the loop graph is instantiated once per engine and configuration
   cudaGraph_t loop_graph = nullptr;
   cudaGraphExec_t loop_exec = nullptr;
@@ -292,14 +412,18 @@ struct Engine::Impl {
   }
 
   // algorithmic work of one score launch: flops and bytes
-  void score_work(long long c0, long long c1, double& flops, double& bytes) const {
+  // only: 0 every candidate, 1 those with |phi(r)| = 1, 2 those with |phi(r)| >= 2
+  void score_work(long long c0, long long c1, double& flops, double& bytes, int only = 0) const {
     long long R = 0;
     for (int i : hs.supernodes) R += PhaseMask{prob.mask[size_t(i)]}.count();
     const long long ns = (long long)hs.supernodes.size();
     std::set<int> cols;
     flops = 0;
+    long long nc = 0;
     for (long long c = c0; c < c1; ++c) {
       const int q = PhaseMask{prob.mask[size_t(cr[size_t(c)])]}.count();
+      if ((only == 1 && q != 1) || (only == 2 && q == 1)) continue;
+      ++nc;
       const double Rp = double(R - q);
       flops += 2.0 * q * Rp + double(L) * ((8.0 * q + 4.0) * Rp + 2.0 * nphi + double(ns - 1));
       cols.insert(cs[size_t(c)]);
@@ -309,8 +433,8 @@ struct Engine::Impl {
     for (int node : cols) zc += PhaseMask{prob.mask[size_t(node)]}.count();
     bytes = 16.0 * double(zc) * double(R)               // Z columns of every endpoint over active rows
             + double(L) * double(R) * 32.0              // base + cluster min/max
-            + double(c1 - c0) * (16.0 + 48.0 * L)       // candidates + i_agg of r
-            + 4.0 * double(ns) + 16.0 * double(c1 - c0) * L;  // super-node table + outputs
+            + double(nc) * (16.0 + 48.0 * L)            // candidates + i_agg of r
+            + 4.0 * double(ns) + 16.0 * double(nc) * L;  // super-node table + outputs
   }
 
   // ---- elimination schedules -----------------------------------------------
@@ -901,6 +1025,7 @@ struct Engine::Impl {
     CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     CK(cudaMallocHost(&h_fail, sizeof(unsigned long long)));
     CK(cudaDeviceGetAttribute(&optin_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    parse_s1_gk();
     for (auto fn : {csolve_kernel<CM_FULL>, csolve_kernel<CM_BASE>, csolve_kernel<CM_ZCOL>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     for (auto fn : {csolve_warp_kernel<CM_FULL, true>, csolve_warp_kernel<CM_BASE, true>,
@@ -1006,7 +1131,7 @@ struct Engine::Impl {
     d_tfwd.alloc(size_t(L) * std::max(nphi, 1));
     d_psmice.alloc(size_t(s3_ldc()) * L);
     d_pmaxerr.alloc(size_t(s3_ldc()) * L);
-    d_grpdone.alloc(size_t(s3_ldc()) / 4 + 8);
+    d_grpdone.alloc(s3_groups_max());
     CK(cudaMemset(d_grpdone.p, 0, d_grpdone.n * sizeof(int)));
     d_pcand.alloc(size_t(2 * n));
     d_best.alloc(size_t(2 + L));
@@ -1037,6 +1162,10 @@ struct Engine::Impl {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
+    if (stream3) cudaStreamDestroy(stream3);
+    if (stream_cap) cudaStreamDestroy(stream_cap);
+    if (ev_fork3) cudaEventDestroy(ev_fork3);
+    if (ev_join3) cudaEventDestroy(ev_join3);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -1220,14 +1349,45 @@ struct Engine::Impl {
       S3Args q = s3_args();
       q.C = int(C);
       q.R = R;
+      q.S = s3_lanes(C * L, s3_fill(), s3_force);
       int c3 = 0;
       for (int k = 1; k <= 3; ++k) {
+        const int cpc = !s1_ok() ? s3_cpc(s3_slots(), k, q.S)
+                                 : (k == 1 ? s1_gk[s1_switch_index(q.S)] : s3_cpc(s3_slots(), k, q.s_multi));
         q.grp_start[k] = grp_off[k - 1];
         q.grp_cta[k - 1] = c3;
-        c3 += (grp_off[k] - grp_off[k - 1] + s3_slots() / k - 1) / (s3_slots() / k) * q.nsl;
+        c3 += (grp_off[k] - grp_off[k - 1] + cpc - 1) / cpc * q.nsl;
       }
       q.grp_cta[3] = c3;
-      if (c3 > 0) {
+      if (s1_ok()) {
+        launch_s1(q.S, q, q.grp_cta[1], stream);
+        if (profile) {  // score1 timed on its own (the roofline kernel); score3's share below
+          const float ms = event_ms();
+          double f, b;
+          score_work(score_c0, score_c0 + C, f, b, 1);
+          score_stats.launches += 1;
+          score_stats.ms += ms;
+          score_stats.flops += f;
+          score_stats.bytes += b;
+          CK(cudaEventRecord(ev_a, stream));
+        }
+        q.skip_nl1 = 1;
+        if (c3 > q.grp_cta[1]) {
+          score3_kernel<<<c3 - q.grp_cta[1], s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
+          launched();
+          CK(cudaGetLastError());
+        }
+        if (profile) {
+          const float ms = event_ms();
+          double f, b;
+          score_work(score_c0, score_c0 + C, f, b, 2);
+          multi_stats.launches += c3 > q.grp_cta[1] ? 1 : 0;
+          multi_stats.ms += ms;
+          multi_stats.flops += f;
+          multi_stats.bytes += b;
+        }
+        return;
+      } else if (c3 > 0) {
         score3_kernel<<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
         launched();
         CK(cudaGetLastError());
@@ -1363,7 +1523,11 @@ struct Engine::Impl {
     a.kcap = int(enum_kcap());
     a.inc_enum = std::getenv("KRONRED_ENUM_FULL") == nullptr ? 1 : 0;
     a.nsl = s3_nsl();
-    for (int k = 1; k <= 3; ++k) a.cpc[k] = s3_slots() / k;
+    a.G3 = s3_slots();
+    for (int i = 0; i < 3; ++i) a.gk1[i] = s1_ok() ? s1_gk[i] : 0;
+    a.s_multi = s3_multi_lanes();
+    a.fill = s3_fill();
+    a.force_s = s3_force;
     a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
     a.has_target = cfg.target_reduction ? 1 : 0;
     a.target = cfg.target_reduction ? *cfg.target_reduction : 0.0;
@@ -1517,14 +1681,50 @@ struct Engine::Impl {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score3_kernel, s3_threads(), sm3));
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-      const int items_max = ((2 * nb + 4) / 5 + 3) * s3_nsl();
+      const int items_max = 4 * ((2 * nb + 4) / 5 + 3) * s3_nsl();  // up to 4 lanes per pair
       const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
+      const bool s1 = s1_ok();
+      // one switch handle per unrolled copy (a handle drives one conditional
+      // node); the enumeration of copy u sets copy u + 1's
+      cudaGraphConditionalHandle hsw[kLoopUnroll] = {};
+      if (s1) {
+        // first iteration's split: the candidate count of iteration 1 is a
+        // property of the network (the graph is keyed on it)
+        std::vector<int> c0s, c0r;
+        hs.enumerate(c0s, c0r);
+        const int S0 = s3_lanes((long long)c0s.size() * L, s3_fill(), s3_force);
+        for (int u = 0; u < kLoopUnroll; ++u)
+          CK(cudaGraphConditionalHandleCreate(&hsw[u], body, unsigned(u == 0 ? s1_switch_index(S0) : 0),
+                                              cudaGraphCondAssignDefault));
+        lb.use_scond = 1;
+        q.skip_nl1 = 1;
+        if (!stream3) {
+          CK(cudaStreamCreateWithFlags(&stream3, cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&ev_fork3, cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&ev_join3, cudaEventDisableTiming));
+        }
+      }
       for (int u = 0; u < kLoopUnroll; ++u) {
-      launch_dep(pdl && pdl_score, score3_kernel, dim3(grid3), dim3(s3_threads()), sm3, stream, q);
+      if (s1) {
+        // |phi(r)| >= 2 candidates (score3) next to the |phi(r)| = 1 ones
+        // (score1<S>, S picked by the enumeration through a switch node)
+        CK(cudaEventRecord(ev_fork3, stream));
+        CK(cudaStreamWaitEvent(stream3, ev_fork3, 0));
+        score3_kernel<<<grid3, s3_threads(), sm3, stream3>>>(q);
+        lb.scond = hsw[(u + 1) % kLoopUnroll];  // set by this copy's enumeration
+        add_switch(stream, hsw[u], [&](int i, cudaStream_t cs) {
+          const int Si = i == 0 ? 1 : (i == 1 ? 2 : 4);
+          launch_s1(Si, q, s1_grid(Si, items_max), cs);
+        });
+        CK(cudaEventRecord(ev_join3, stream3));
+        CK(cudaStreamWaitEvent(stream, ev_join3, 0));
+      } else {
+        launch_dep(pdl && pdl_score, score3_kernel, dim3(grid3), dim3(s3_threads()), sm3, stream, q);
+      }
       // pick and refresh follow their stream predecessor by programmatic
       // dependent launch (launch overlapped with the predecessor's tail; each
       // waits on griddepcontrol before reading its results)
-      launch_dep(pdl, pick_commit_kernel, dim3(1), dim3(kLoopThreads), 0, stream, lb);
+      launch_dep(pdl && !s1, pick_commit_kernel, dim3(1), dim3(kLoopThreads), 0, stream, lb);
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
       enum_kernel<<<1, kLoopThreads, enum_smem(), stream2>>>(lb);
@@ -1572,7 +1772,8 @@ struct Engine::Impl {
     CK(cudaStreamSynchronize(stream));
     check_deferred_fail();
     const LoopState st = *h_loopst;
-    launches += 4LL * ((st.iter + kLoopUnroll) / kLoopUnroll * kLoopUnroll);
+    // kernels per loop-body iteration: scorer(s), pick, enumeration, refresh
+    launches += (s1_ok() ? 5LL : 4LL) * ((st.iter + kLoopUnroll) / kLoopUnroll * kLoopUnroll);
     const int it = st.iter;
     if (loop_trace && it > 2) {
       std::vector<unsigned long long> T(size_t(n + 1) * kTdbg);
@@ -1660,8 +1861,11 @@ void Engine::set_profile(bool on) {
   impl_->profile = on;
   impl_->score_stats = KernelStats{};
   impl_->solve_stats = KernelStats{};
+  impl_->multi_stats = KernelStats{};
 }
-KernelStats Engine::stats(int which) const { return which == 0 ? impl_->score_stats : impl_->solve_stats; }
+KernelStats Engine::stats(int which) const {
+  return which == 0 ? impl_->score_stats : (which == 1 ? impl_->solve_stats : impl_->multi_stats);
+}
 const Problem& Engine::problem() const { return impl_->prob; }
 std::int64_t Engine::launches() const { return impl_->launches; }
 

@@ -45,6 +45,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 
 struct LoopState {
   int done, iter, ns, C, R, err;
+  int S;             // scorer lanes per (candidate, scenario) pair this iteration
   int last_s, last_r;  // the last committed candidate (incremental base refresh)
   int grp_start[4];  // candidate offset of each |phi(r)| group (index 1..3)
   int grp_cta[4];    // first CTA of each group; grp_cta[3] = CTAs in use

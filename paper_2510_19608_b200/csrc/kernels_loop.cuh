@@ -30,7 +30,11 @@ namespace {
 struct LoopArgs {
   LoopState* st;
   int n, nb, slack, L, nphi, cap;
-  int cpc[4];          // candidates per scorer CTA for each |phi(r)| group (1..3)
+  int G3;              // scorer Z-column slots per CTA (candidates per CTA: s3_cpc(G3, |phi(r)|, S))
+  int gk1[3];          // score1 candidates per CTA at S = 1, 2, 4 (0: score3 takes |phi(r)| = 1 too)
+  int s_multi;         // score3's split for the |phi(r)| >= 2 groups when score1 runs
+  long long fill;      // scorer row split: thread budget (s3_lanes)
+  int force_s;         // scorer row split forced to 1/2/4 (0: automatic)
   int inc_enum;        // 1: incremental candidate list after a commit (else full rebuild)
   int kcap;            // keys region size (power of two >= 2 nb); the previous list follows it
   int nsl;             // scenario slices per candidate group (score3), 1 otherwise
@@ -64,6 +68,8 @@ struct LoopArgs {
   unsigned long long* tr_t;  // [cap] globaltimer at commit
   cudaGraphConditionalHandle cond;
   int use_cond;
+  cudaGraphConditionalHandle scond;  // switch over the scorer's row split (score1<1|2|4>)
+  int use_scond;
   unsigned long long* tdbg;  // optional timeline [iter][8]: pick start/end, enum start/end
 };
 
@@ -490,15 +496,21 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   }
   if (tid == 0) {
     const int cnt3 = C - cnt1 - cnt2;
+    const int S = s3_lanes((long long)C * a.L, a.fill, a.force_s);
+    const int gk1 = a.gk1[S == 1 ? 0 : (S == 2 ? 1 : 2)];
+    const int Sm = gk1 > 0 ? a.s_multi : S;  // split of the |phi(r)| >= 2 groups
+    const int cpc1 = gk1 > 0 ? gk1 : s3_cpc(a.G3, 1, S), cpc2 = s3_cpc(a.G3, 2, Sm), cpc3 = s3_cpc(a.G3, 3, Sm);
+    st->S = S;
     st->C = C;
+    if (a.use_scond) cudaGraphSetConditional(a.scond, S == 1 ? 0u : (S == 2 ? 1u : 2u));
     st->grp_start[0] = 0;
     st->grp_start[1] = 0;
     st->grp_start[2] = cnt1;
     st->grp_start[3] = cnt1 + cnt2;
     st->grp_cta[0] = 0;
-    st->grp_cta[1] = (cnt1 + a.cpc[1] - 1) / a.cpc[1] * a.nsl;
-    st->grp_cta[2] = st->grp_cta[1] + (cnt2 + a.cpc[2] - 1) / a.cpc[2] * a.nsl;
-    st->grp_cta[3] = st->grp_cta[2] + (cnt3 + a.cpc[3] - 1) / a.cpc[3] * a.nsl;
+    st->grp_cta[1] = (cnt1 + cpc1 - 1) / cpc1 * a.nsl;
+    st->grp_cta[2] = st->grp_cta[1] + (cnt2 + cpc2 - 1) / cpc2 * a.nsl;
+    st->grp_cta[3] = st->grp_cta[2] + (cnt3 + cpc3 - 1) / cpc3 * a.nsl;
     if (a.use_cond) cudaGraphSetConditional(a.cond, 1u);
     if (a.tdbg) a.tdbg[size_t(st->iter) * kTdbg + 3] = globaltimer();
 #ifdef ENUM_TIMING

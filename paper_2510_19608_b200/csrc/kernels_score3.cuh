@@ -1,5 +1,6 @@
 // score3: the production magnitude-objective scorer (reduce.cpp:89-123,
-// 194-244). One thread per (candidate, scenario) pair.
+// 194-244). S lanes per (candidate, scenario) pair, S in {1, 2, 4} chosen per
+// iteration from the pair count (row split, below).
 //
 // A CTA owns Gk candidates x Ls scenarios (a scenario slice; Gk = G / |phi(r)|
 // so the staged Z columns always fit G slots) and walks the iteration's row
@@ -24,6 +25,15 @@
 // SMICE sum and the running max_err. Other blocks take the general per-row
 // path; a block whose |Vc|^2 leaves the fast sqrt range is redone with
 // __dsqrt_rn.
+//
+// Row split. A tile is four 4-row passes. With S lanes per pair (adjacent
+// lanes of one warp), lane q computes passes q, q + S, ... of every tile, so a
+// pair walks its rows S times faster and S times as many warps fill the GPU
+// when the candidate set is small (mid and late iterations). The ordered
+// SMICE fold stays one left-to-right chain: after each round of S passes the
+// owner lanes fold their own rows in pass order, handing (smice, cm) on by
+// warp shuffle; max_err is an order-free maximum, reduced over the S lanes at
+// the end. Every rounding step is the S = 1 program's.
 #pragma once
 
 namespace kronred::b200 {
@@ -33,7 +43,11 @@ constexpr int K3 = 16;  // rows per tile
 
 struct S3Args {
   int C, L, nphi, R;
-  int G;                     // Z column slots per CTA (candidates per CTA = G / |phi(r)|)
+  int G;                     // Z column slots per CTA (candidates per CTA = G / |phi(r)| / S)
+  int S;                     // lanes per pair (host-driven loop; the device loop reads st->S)
+  int ns_max;                // staging ring: most slots an item may carve (>= 3)
+  int skip_nl1;              // 1: leave the |phi(r)| = 1 items to score1_kernel
+  int s_multi;               // lanes per pair of the |phi(r)| >= 2 items when skip_nl1
   int Ls, nsl;               // scenario slice width and slice count
   const int4* cand;          // grouped by |phi(r)|: (s, r, table row of s, table row of r)
   const int* cand_idx;       // lexicographic index of each grouped slot
@@ -73,12 +87,6 @@ struct S3Layout {
 #ifndef S3_MIN_BLOCKS  // tuning: resident CTAs the register budget is sized for
 #define S3_MIN_BLOCKS 3
 #endif
-#ifndef S3_NRT1  // tuning: rows per straight-line pass for single-phase candidates
-#define S3_NRT1 4
-#endif
-#ifndef S3_HH_UNROLL
-#define S3_HH_UNROLL 0
-#endif
 
 // max(a, b) for the scorer's error terms. Every call has at least one operand
 // >= +0 (em = max(m - lo, hi - m) with lo <= hi: if m < lo then hi - m > 0;
@@ -110,12 +118,10 @@ __device__ __forceinline__ double s3_tree_max(const double (&em)[NR]) {
   return t[0];
 }
 
-// NR plain rows: Vc, |Vc|, exact cluster error, then NR super-node
-// boundaries of the ordered fold (ILP NR until the fold).
+// NR plain rows: Vc, |Vc| and the exact cluster error of each row (ILP NR).
 template <int NL, int NR>
-__device__ __forceinline__ void s3_plain(const double2* __restrict__ bvp, const double2* __restrict__ zp, int RS,
-                                         int u0, const C2 (&cv)[NL], double& smice, double& cm, double& mx) {
-  double em[NR];
+__device__ __forceinline__ void s3_plain_em(const double2* __restrict__ bvp, const double2* __restrict__ zp, int RS,
+                                            int u0, const C2 (&cv)[NL], double (&em)[NR]) {
   bool bad = false;
 #pragma unroll
   for (int v = 0; v < NR; ++v) {
@@ -147,12 +153,16 @@ __device__ __forceinline__ void s3_plain(const double2* __restrict__ bvp, const 
       em[v] = s3max(dev::dsub(m, b1.x), dev::dsub(b1.y, m));
     }
   }
+}
+
+// the ordered fold over NR plain rows (every row a super-node boundary)
+template <int NR>
+__device__ __forceinline__ void s3_fold_plain(const double (&em)[NR], double& smice, double& cm) {
 #pragma unroll
   for (int v = 0; v < NR; ++v) {
     smice = dev::dadd(smice, cm);
     cm = em[v];
   }
-  mx = s3max(mx, s3_tree_max(em));
 }
 
 __device__ __forceinline__ bool s3_block_plain(uint4 e4) {
@@ -203,10 +213,9 @@ struct S3Fix {
 // A zero current c_p adds (+-0) to Vc, which leaves |Vc| bit-identical for
 // finite Z, so the reference's skip (reduce.cpp:227) needs no branch here.
 template <int NL, int NR>
-__device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, const double2* __restrict__ zp, int RS,
-                                            int u0, int t0, const unsigned* tb, const C2 (&cv)[NL], const S3Fix& f,
-                                            double& smice, double& cm, double& mx) {
-  double em[NR];
+__device__ __forceinline__ void s3_rows_gen_em(const double2* __restrict__ bvp, const double2* __restrict__ zp,
+                                               int RS, int u0, int t0, const unsigned* tb, const C2 (&cv)[NL],
+                                               const S3Fix& f, double (&em)[NR]) {
   bool bad = false;
   auto fix = [&](int v, double m, double e) {
     const int t = t0 + u0 + v;
@@ -248,6 +257,12 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
       em[v] = fix(v, m, s3max(dev::dsub(m, b1.x), dev::dsub(b1.y, m)));
     }
   }
+}
+
+// the ordered fold over NR general rows, driven by the first-of-super-node bit
+template <int NR>
+__device__ __forceinline__ void s3_fold_gen(const double (&em)[NR], const unsigned* tb, int u0, double& smice,
+                                            double& cm) {
 #pragma unroll
   for (int v = 0; v < NR; ++v) {
     if (tb[u0 + v] & 4u) {
@@ -256,30 +271,48 @@ __device__ __forceinline__ void s3_rows_gen(const double2* __restrict__ bvp, con
     }
     cm = s3max(cm, em[v]);
   }
-  mx = s3max(mx, s3_tree_max(em));
 }
 
-template <int NL, int LSC>  // LSC: compile-time slice width (0: runtime a.Ls)
-__device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin, int g_count, int R, double* smd,
-                                        int g_base_group) {
+// (smice, cm) of lane q of this lane's S-lane group, to every lane of the group
+__device__ __forceinline__ void s3_handoff(double& smice, double& cm, int q, int S) {
+  const int src = (int(threadIdx.x & 31u) & ~(S - 1)) | q;
+  smice = __shfl_sync(0xffffffffu, smice, src);
+  cm = __shfl_sync(0xffffffffu, cm, src);
+}
+
+// candidates per CTA of the |phi(r)| = NL group at S lanes per pair
+__host__ __device__ __forceinline__ int s3_cpc(int G, int NL, int S) { return G / NL / S > 1 ? G / NL / S : 1; }
+
+// One work item (a group of candidates x one scenario slice). SF = 1: the
+// one-lane-per-pair program compiled on its own (S = 1); SF = 0: S lanes per
+// pair from the argument.
+template <int NL, int LSC, int SF>  // LSC: compile-time slice width (0: runtime a.Ls)
+__device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, int g_begin, int g_count, int R,
+                                     double* smd, int g_base_group) {
+  const int S = SF ? 1 : S_arg;
   const int L = a.L, Ls = LSC ? LSC : a.Ls;
-  const int Gk = a.G / NL;
+  const int Gk = s3_cpc(a.G, NL, S);
   const int P = blockDim.x;
   const int tid = threadIdx.x;
+  const int pr = tid / S, myq = tid - pr * S;  // pair slot, lane within the pair's group
   const int cgrp = local / a.nsl, sl = local - cgrp * a.nsl;
-  const int gl = min(tid / Ls, Gk - 1);
-  const int ll = tid - (tid / Ls) * Ls;
+  const int gl = min(pr / Ls, Gk - 1);
+  const int ll = pr - (pr / Ls) * Ls;
   const int l = min(sl * Ls + ll, L - 1);
   const int cg = cgrp * Gk + gl;
-  const bool valid = tid < Gk * Ls && cg < g_count && sl * Ls + ll < L;
+  const bool valid = pr < Gk * Ls && cg < g_count && sl * Ls + ll < L && myq == 0;
   const int c = g_begin + min(cg, g_count - 1);
   const S3Layout lay{Ls, a.G};
   double2* base2 = reinterpret_cast<double2*>(smd);
-  const size_t buf_e = lay.buf_e();
+  // staging ring: the allocation holds 3 slots of the widest item (G Z-column
+  // slots); an item with fewer candidates (row split) carves it into more,
+  // smaller slots, so more tiles are in flight while a slot computes
+  const size_t buf_e = lay.tab_e() + lay.bv_e() + size_t(Gk) * (NL * 2 * K3 + 1);
+  const int NS = max(3, min(a.ns_max, int(3 * lay.buf_e() / buf_e)));
   auto tab_s = [&](int b) { return reinterpret_cast<unsigned*>(base2 + b * buf_e); };
   auto bv_s = [&](int b) { return base2 + b * buf_e + lay.tab_e(); };
   auto z_s = [&](int b) { return base2 + b * buf_e + lay.tab_e() + lay.bv_e(); };
-  int* zcol = reinterpret_cast<int*>(base2 + 3 * buf_e);  // [Gk][NL][2]
+  int* zcol = reinterpret_cast<int*>(base2 + 3 * lay.buf_e());  // [Gk][NL][2]
 
   const int4 cd = a.cand[c];
   const int s = cd.x, r = cd.y;
@@ -304,7 +337,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
 #pragma unroll
       for (int k = 0; k < NL; ++k)
         if (k == j) cv[k] = cz;
-      if (ll == 0 && tid < Gk * Ls) {
+      if (ll == 0 && myq == 0 && pr < Gk * Ls) {
         zcol[(gl * NL + j) * 2 + 0] = rs0 + popc_below(ms, ph);
         zcol[(gl * NL + j) * 2 + 1] = rr;
       }
@@ -426,22 +459,21 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
 #ifdef S3_TIMING  // tuning aid: per-phase cycle counts of CTA 0's warps
   long long tm_pro = clock64(), tm_wait = 0, tm_stage = 0, tm_rho = 0, tm_fd = 0, tm_comp = 0, tm_x;
 #endif
-  if (fst) {
-    unsigned r0[3], r1[3];
-    load_rho(0, r0);
-    load_rho(1, r1);
-    stage_fast(0, 0, r0);
-    cp_async_commit();
-    if (ntiles > 1) stage_fast(1, 1, r1);
-    cp_async_commit();
-    load_rho(2, rn);
-  } else {
-    stage(0, 0);
-    cp_async_commit();
-    if (ntiles > 1) stage(1, 1);
+  // prologue: tiles 0 .. NS-2 in flight (one commit group each, empty past
+  // the end), then wait for tile 0
+  for (int t = 0; t < NS - 1; ++t) {
+    if (t < ntiles) {
+      if (fst) {
+        load_rho(t, rn);
+        stage_fast(t, t, rn);
+      } else {
+        stage(t, t);
+      }
+    }
     cp_async_commit();
   }
-  cp_async_wait1();
+  if (fst) load_rho(NS - 1, rn);
+  cp_async_wait_pending(NS - 2);
   __syncthreads();
   form_d(0);
 #ifdef S3_TIMING
@@ -449,39 +481,39 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
 #endif
   unsigned tflag_next = a.tplain[0];  // raw byte: tested one tile later
   for (int j = 0; j < ntiles; ++j) {
-    const int b = j % 3;
+    const int b = j % NS;
     const bool tflag = tflag_next != 0u;
     if (j + 1 < ntiles) tflag_next = a.tplain[j + 1];
 #ifdef S3_TIMING
     tm_x = clock64();
 #endif
-    asm volatile("cp.async.wait_group 0;\n" ::);
+    cp_async_wait_pending(NS - 3);  // tile j + 1 has landed; tiles j + 2 .. j + NS - 2 may be in flight
     __syncthreads();
 #ifdef S3_TIMING
     tm_wait += clock64() - tm_x;
     tm_x = clock64();
 #endif
     if (fst) {
-      if (j + 2 < ntiles) stage_fast(j + 2, (j + 2) % 3, rn);
+      if (j + NS - 1 < ntiles) stage_fast(j + NS - 1, (j + NS - 1) % NS, rn);
       cp_async_commit();
 #ifdef S3_TIMING
       tm_stage += clock64() - tm_x;
       tm_x = clock64();
 #endif
-      load_rho(j + 3, rn);  // consumed next iteration: latency hidden by this tile's compute
+      load_rho(j + NS, rn);  // consumed next iteration: latency hidden by this tile's compute
 #ifdef S3_TIMING
       tm_rho += clock64() - tm_x;
       tm_x = clock64();
 #endif
     } else {
-      if (j + 2 < ntiles) stage(j + 2, (j + 2) % 3);
+      if (j + NS - 1 < ntiles) stage(j + NS - 1, (j + NS - 1) % NS);
       cp_async_commit();
     }
 #ifdef S3_TIMING
     tm_stage += clock64() - tm_x;
     tm_x = clock64();
 #endif
-    if (j + 1 < ntiles) form_d((j + 1) % 3);
+    if (j + 1 < ntiles) form_d((j + 1) % NS);
 #ifdef S3_TIMING
     tm_fd += clock64() - tm_x;
     tm_x = clock64();
@@ -494,26 +526,55 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
     // this warp's candidates: straight-line passes with the all-first fold;
     // any other tile: the same fast passes with per-row fixups and a
     // flag-driven fold
-    constexpr int NRT = NL == 1 ? S3_NRT1 : 4;  // rows per pass (register budget)
-    if (tflag && !__any_sync(0xffffffffu, j == (ts0 >> 4) || j == (tr0 >> 4))) {
-#if S3_HH_UNROLL
-#pragma unroll
-#else
+    // passes of 4 rows; round k, lane q computes pass k * S + q (S = 1: every
+    // pass, in order); the owners then fold in pass order, handing (smice, cm)
+    // on to the next lane of the pair's group
+    const bool plain = tflag && !__any_sync(0xffffffffu, j == (ts0 >> 4) || j == (tr0 >> 4));
+    constexpr int NP = K3 / 4;
+    const int rounds = NP / S;
+    if (plain) {
 #pragma unroll 1
-#endif
-      for (int hh = 0; hh < K3 / NRT; ++hh) s3_plain<NL, NRT>(bvp, zp, RS, NRT * hh, cv, smice, cm, mx);
+      for (int k = 0; k < rounds; ++k) {
+        const int u0 = 4 * (k * S + myq);
+        double em[4];
+        s3_plain_em<NL, 4>(bvp, zp, RS, u0, cv, em);
+        mx = s3max(mx, s3_tree_max(em));
+        if (S == 1) {
+          s3_fold_plain<4>(em, smice, cm);
+        } else {
+#pragma unroll 1
+          for (int q = 0; q < S; ++q) {
+            if (myq == q) s3_fold_plain<4>(em, smice, cm);
+            s3_handoff(smice, cm, q, S);
+          }
+        }
+      }
     } else {
 #pragma unroll 1
-      for (int hh = 0; hh < K3 / NRT; ++hh)
-        s3_rows_gen<NL, NRT>(bvp, zp, RS, NRT * hh, t0, tb, cv, fx, smice, cm, mx);
+      for (int k = 0; k < rounds; ++k) {
+        const int u0 = 4 * (k * S + myq);
+        double em[4];
+        s3_rows_gen_em<NL, 4>(bvp, zp, RS, u0, t0, tb, cv, fx, em);
+        mx = s3max(mx, s3_tree_max(em));
+        if (S == 1) {
+          s3_fold_gen<4>(em, tb, u0, smice, cm);
+        } else {
+#pragma unroll 1
+          for (int q = 0; q < S; ++q) {
+            if (myq == q) s3_fold_gen<4>(em, tb, u0, smice, cm);
+            s3_handoff(smice, cm, q, S);
+          }
+        }
+      }
     }
 #ifdef S3_TIMING
     tm_comp += clock64() - tm_x;
 #endif
   }
   smice = dev::dadd(smice, cm);
+  for (int o = 1; o < S; o <<= 1) mx = s3max(mx, __shfl_xor_sync(0xffffffffu, mx, o));  // order-free
 #ifdef S3_TIMING
-  if (blockIdx.x == 0 && (tid & 31) == 0 && a.st && (a.st->iter == 1 || a.st->iter == 100 || a.st->iter == 850))
+  if (blockIdx.x == 0 && (tid & 31) == 0 && a.st && (a.st->iter == 1 || a.st->iter == 100 || a.st->iter == 500 || a.st->iter == 850))
     printf("s3 timing iter %d warp %d NL %d tiles %d: prologue %lld wait+sync %lld stage %lld rho %lld form_d %lld compute %lld\n",
            a.st->iter, tid >> 5, NL, ntiles, tm_pro, tm_wait, tm_stage, tm_rho, tm_fd, tm_comp);
 #endif
@@ -565,6 +626,15 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int local, int g_begin,
   }
 }
 
+// lanes per pair for an iteration with `pairs` (candidate, scenario) pairs:
+// the widest split that keeps pairs * S within `fill` threads (about one wave)
+__host__ __device__ __forceinline__ int s3_lanes(long long pairs, long long fill, int force) {
+  if (force == 1 || force == 2 || force == 4) return force;
+  if (pairs * 4 <= fill) return 4;
+  if (pairs * 2 <= fill) return 2;
+  return 1;
+}
+
 __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
   extern __shared__ double sm_dyn[];
   const int b = blockIdx.x;
@@ -584,17 +654,21 @@ __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
     gs = a.st->grp_start;
     gc = a.st->grp_cta;
   }
+  // with score1 taking the |phi(r)| = 1 candidates, the few multi-phase ones
+  // run at their own split (latency-bound: one pass per lane per tile)
+  const int S = a.skip_nl1 ? a.s_multi : (a.st ? a.st->S : a.S);
   // work items (candidate group x scenario slice) strided over the grid: the
   // device loop launches a fixed, occupancy-sized grid for every iteration
-  for (int w = b; w < gc[3]; w += gridDim.x) {
+  // (skip_nl1: the |phi(r)| = 1 items run in score1_kernel)
+  for (int w = b + (a.skip_nl1 ? gc[1] : 0); w < gc[3]; w += gridDim.x) {
     // counter slot: global candidate-group index (every group range is a
     // whole number of nsl-slice items)
     if (w < gc[1])
-      s3_body<1, 0>(a, w, gs[1], gs[2] - gs[1], R, sm_dyn, 0);
+      s3_body<1, 0, 0>(a, S, w, gs[1], gs[2] - gs[1], R, sm_dyn, 0);
     else if (w < gc[2])
-      s3_body<2, 0>(a, w - gc[1], gs[2], gs[3] - gs[2], R, sm_dyn, gc[1] / a.nsl);
+      s3_body<2, 0, 0>(a, S, w - gc[1], gs[2], gs[3] - gs[2], R, sm_dyn, gc[1] / a.nsl);
     else
-      s3_body<3, 0>(a, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
+      s3_body<3, 0, 0>(a, S, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
     __syncthreads();  // shared memory is reused by the next item
   }
 }

@@ -328,3 +328,19 @@ def test_cpp_state_invariants_and_kron_consistency(case, e_bar, tmp_path):
                        capture_output=True, text=True)
     assert p.returncode == 0, p.stdout + p.stderr
     assert "failures 0" in p.stdout
+
+
+@pytest.mark.parametrize("S", [1, 2, 4])
+@pytest.mark.parametrize("case,tag,e_bar", [("c2", "mag_3e-3", 3e-3), ("h2k", "mag_3e-3", 3e-3),
+                                            ("m40", "mag_1e-3", 1e-3), ("c1", "mag_1e-2", 1e-2)])
+def test_scorer_row_split_bitwise(S, case, tag, e_bar, monkeypatch, tmp_path):
+    """Row split (KRONRED_S3_S: 1, 2 or 4 lanes per (candidate, scenario)
+    pair, the ordered SMICE fold handed from lane to lane) reproduces the
+    reference's trajectory and reduced model bit for bit, on the benchmark
+    feeder, the three-phase-heavy feeder (|phi(r)| = 2, 3 groups) and C1."""
+    monkeypatch.setenv("KRONRED_S3_S", str(S))
+    res = kr.Context(host(case)).run_reduction(kr.ReductionConfig(e_bar=e_bar))
+    assert_trace(res, case, tag)
+    out = tmp_path / "r.json"
+    res.write_reduced_json(str(out))
+    assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
