@@ -211,6 +211,10 @@ using IterationObserver = std::function<void(const AssignmentState&, const Trace
 ReductionResult run_reduction(const Network& net, const ScenarioLibrary& lib,
                               const ReductionConfig& cfg,
                               const IterationObserver& observer = {});
+/// The device engine behind run_reduction / model_max_errors is cached per
+/// calling thread and reused for networks of the same structure (values are
+/// re-uploaded; KRONRED_ENGINE_CACHE=0 disables). Frees it.
+void release_engine_cache();
 
 // --- Kron (kron.hpp:13-49) --------------------------------------------------
 struct Partition {

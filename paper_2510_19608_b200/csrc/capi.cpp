@@ -338,6 +338,53 @@ int device_from_env() {
   return -1;  // current device of the calling thread
 }
 
+// Engine cache of the C++ drop-in entry points (one per calling thread): the
+// reference signature builds its solver per call (reduce.cpp:359); here a call
+// on a network of the same STRUCTURE (node phases, slack, branch endpoints,
+// block pattern, scenario count, device) reuses the resident engine -- its
+// elimination schedule, device allocations and instantiated loop graph -- and
+// only re-uploads the values (Engine::reload + set_scenarios: H2D copies and
+// the refactorization every run performs anyway). KRONRED_ENGINE_CACHE=0
+// disables it; kronred::release_engine_cache() frees it.
+struct EngineCache {
+  std::string key;
+  std::unique_ptr<Engine> eng;
+};
+thread_local EngineCache t_engine_cache;
+
+std::string structure_key(const Problem& p, int device) {
+  std::string k;
+  auto put = [&](const void* d, size_t n) { k.append(static_cast<const char*>(d), n); };
+  const int hdr[4] = {p.y.n, p.slack, p.L, device};
+  put(hdr, sizeof hdr);
+  put(p.mask.data(), p.mask.size());
+  put(p.y.row.data(), p.y.row.size() * sizeof(int));
+  put(p.y.col.data(), p.y.col.size() * sizeof(int));
+  for (const Branch& b : p.net.branches) {
+    const int e[2] = {b.from, b.to};
+    put(e, sizeof e);
+  }
+  return k;
+}
+
+// the engine for `p`: the cached one with new values, or a new one
+Engine& cached_engine(const Problem& p) {
+  const int dev = device_from_env();
+  const char* e = std::getenv("KRONRED_ENGINE_CACHE");
+  const bool on = !(e && std::string(e) == "0");
+  std::string key = structure_key(p, dev);
+  EngineCache& c = t_engine_cache;
+  if (on && c.eng && c.key == key) {
+    c.eng->reload(p);
+    c.eng->set_scenarios(p.scenario_ids, p.injections, p.voltages);
+    return *c.eng;
+  }
+  c.eng.reset();  // release the old device memory before allocating
+  c.eng = std::make_unique<Engine>(p, dev);
+  c.key = on ? std::move(key) : std::string();
+  return *c.eng;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -373,7 +420,7 @@ ReductionResult run_reduction(const Network& net, const ScenarioLibrary& lib, co
   if (!(cfg.e_bar >= 0)) throw ConfigError("e_bar must be non-negative");
   if (cfg.target_reduction && !(*cfg.target_reduction >= 0 && *cfg.target_reduction <= 1))
     throw ConfigError("target_reduction must lie in [0,1]");
-  Engine eng(problem_from(net, &lib), device_from_env());
+  Engine& eng = cached_engine(problem_from(net, &lib));
   ResultData rd;
   Engine::Observer obs;
   if (observer) obs = [&](const HostState& hs, const TraceRow& row) { observer(hs, row); };
@@ -404,8 +451,12 @@ KronResult kron_reduce(const BlockMatrix& y, const std::vector<PhaseMask>& phase
 }
 
 std::vector<double> model_max_errors(const ReducedModel& model, const Network& net, const ScenarioLibrary& lib) {
-  Engine eng(problem_from(net, &lib), device_from_env());
-  return eng.model_errors(model);
+  return cached_engine(problem_from(net, &lib)).model_errors(model);
+}
+
+void release_engine_cache() {
+  t_engine_cache.eng.reset();
+  t_engine_cache.key.clear();
 }
 
 ReducedModel radialize(const ReducedModel& model, const Network& original, const BlockMatrix& y,

@@ -34,6 +34,9 @@
 #include <numeric>
 #include <set>
 #include <stdexcept>
+#include <atomic>
+#include <functional>
+#include <thread>
 
 #include "kr_device.cuh"
 #include "kr_internal.hpp"
@@ -388,6 +391,7 @@ struct Engine::Impl {
   static constexpr int kLoopKeyBufs = 18;
   const void* loop_key_bufs[kLoopKeyBufs] = {};
   int loop_key_L = -1;
+  bool loop_key_live = false;
   DBuf<unsigned long long> d_tdbg;
   bool loop_trace = std::getenv("KRONRED_LOOP_TRACE") != nullptr;
   bool force_host_loop = std::getenv("KRONRED_LOOP") != nullptr && std::string(std::getenv("KRONRED_LOOP")) == "host";
@@ -1153,6 +1157,7 @@ struct Engine::Impl {
     if (h_fail) cudaFreeHost(h_fail);
     if (h_loopst) cudaFreeHost(h_loopst);
     if (h_trace) cudaFreeHost(h_trace);
+    if (h_live) cudaFreeHost(h_live);
     if (h_cand) cudaFreeHost(h_cand);
     if (h_snt) cudaFreeHost(h_snt);
     if (h_tab) cudaFreeHost(h_tab);
@@ -1576,8 +1581,15 @@ struct Engine::Impl {
 
   // After begin(): runs every iteration on the device (one graph launch with
   // a conditional WHILE node) and returns the committed trace.
+  // live: a row callback (s, r, candidates, smice, max_err[L], wall_ms) invoked
+  // on the calling thread while the graph runs, in commit order; the returned
+  // arrays are then left empty
+  using LiveFn = std::function<void(int, int, int, double, const double*, double)>;
+  char* h_live = nullptr;  // mapped host memory: count + rows
+  size_t h_live_cap = 0;
   void run_device_loop(std::vector<int>& tr_s, std::vector<int>& tr_r, std::vector<int>& tr_c,
-                       std::vector<double>& tr_smice, std::vector<double>& tr_me, std::vector<double>& tr_ms) {
+                       std::vector<double>& tr_smice, std::vector<double>& tr_me, std::vector<double>& tr_ms,
+                       const LiveFn* live = nullptr) {
     const int nb = int(prob.net.branches.size());
     if (!stream2) {
       CK(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
@@ -1620,6 +1632,29 @@ struct Engine::Impl {
       CK(cudaMemcpyAsync(d_loopst.p, &st0, sizeof st0, cudaMemcpyHostToDevice, stream));
     }
     LoopArgs la = loop_args();
+    // live rows: [count (64 B)] [src cap*3 int] [smice cap] [me cap*L] [t cap]
+    const size_t live_bytes = 64 + size_t(n) * (3 * sizeof(int) + sizeof(double) * (1 + size_t(L)) + 8) + 64;
+    if (live) {
+      if (!h_live || h_live_cap < live_bytes) {
+        if (h_live) CK(cudaFreeHost(h_live));
+        h_live = nullptr;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_live), live_bytes, cudaHostAllocMapped));
+        h_live_cap = live_bytes;
+      }
+      std::memset(h_live, 0, 64);
+      char* dp = nullptr;
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), h_live, 0));
+      size_t o = 64;
+      la.live_count = reinterpret_cast<volatile int*>(dp);
+      la.live_src = reinterpret_cast<int*>(dp + o);
+      o += size_t(n) * 3 * sizeof(int);
+      o = (o + 7) & ~size_t(7);
+      la.live_smice = reinterpret_cast<double*>(dp + o);
+      o += size_t(n) * sizeof(double);
+      la.live_me = reinterpret_cast<double*>(dp + o);
+      o += size_t(n) * L * sizeof(double);
+      la.live_t = reinterpret_cast<unsigned long long*>(dp + o);
+    }
     if (loop_trace) {
       d_tdbg.alloc(size_t(n + 1) * kTdbg);
       CK(cudaMemsetAsync(d_tdbg.p, 0, sizeof(unsigned long long) * size_t(n + 1) * kTdbg, stream));
@@ -1647,6 +1682,7 @@ struct Engine::Impl {
                                       d_Z.p,    d_psmice.p, d_grpdone.p, d_loopst.p, d_trme.p, d_sup.p};
     const bool key_ok = loop_exec && loop_key_ebar == cfg.e_bar && loop_key_has == la.has_target &&
                         loop_key_target == la.target && loop_key_trace == loop_trace && loop_key_L == L &&
+                        loop_key_live == (la.live_count != nullptr) &&
                         std::equal(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     if (!key_ok) {
       if (loop_exec) CK(cudaGraphExecDestroy(loop_exec));
@@ -1744,11 +1780,42 @@ struct Engine::Impl {
       loop_key_target = la.target;
       loop_key_trace = loop_trace;
       loop_key_L = L;
+      loop_key_live = la.live_count != nullptr;
       std::copy(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     }
     // the whole loop: one graph launch (a loop that is already done runs one
     // body of early-exit kernels); results come back with one sync
     CK(cudaGraphLaunch(loop_exec, stream));
+    if (live) {
+      // deliver rows as the device publishes them (mapped memory, polled)
+      const volatile int* cnt = reinterpret_cast<const volatile int*>(h_live);
+      const int* src = reinterpret_cast<const int*>(h_live + 64);
+      size_t o = 64 + size_t(n) * 3 * sizeof(int);
+      o = (o + 7) & ~size_t(7);
+      const double* smv = reinterpret_cast<const double*>(h_live + o);
+      const double* mev = reinterpret_cast<const double*>(h_live + o + size_t(n) * sizeof(double));
+      const unsigned long long* tv =
+          reinterpret_cast<const unsigned long long*>(h_live + o + size_t(n) * sizeof(double) * (1 + size_t(L)));
+      int done = 0;
+      unsigned long long tprev = 0;  // iteration 1: from the loop start the first enumeration stamps
+      for (int k = 0; k < 1000 && tprev == 0; ++k) {
+        tprev = *reinterpret_cast<const volatile unsigned long long*>(h_live + 8);
+        if (tprev == 0) std::this_thread::sleep_for(std::chrono::microseconds(5));
+      }
+      for (;;) {
+        const cudaError_t q = cudaStreamQuery(stream);
+        if (q != cudaSuccess && q != cudaErrorNotReady) CK(q);
+        const int c = *cnt;
+        std::atomic_thread_fence(std::memory_order_acquire);
+        for (; done < c; ++done) {
+          const double wall = tprev ? double(tv[done] - tprev) * 1e-6 : 0.0;
+          tprev = tv[done];
+          (*live)(src[3 * done], src[3 * done + 1], src[3 * done + 2], smv[done], mev + size_t(done) * L, wall);
+        }
+        if (q == cudaSuccess && *cnt == done) break;
+        if (q != cudaSuccess) std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+    }
     if (!h_loopst) CK(cudaMallocHost(&h_loopst, sizeof(LoopState)));
     if (!h_trace || h_trace_cap < trace_bytes()) {  // a reload may bring more scenarios
       if (h_trace) CK(cudaFreeHost(h_trace));
@@ -2122,7 +2189,27 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
     // afterwards to rebuild clusters and call the observer in order
     std::vector<int> ts, tr, tc;
     std::vector<double> tsm, tme, tms;
-    I.run_device_loop(ts, tr, tc, tsm, tme, tms);
+    const char* om = std::getenv("KRONRED_OBSERVER");
+    const bool live = obs && !(om && std::string(om) == "replay");
+    Impl::LiveFn deliver = [&](int s, int r, int c, double smice, const double* me, double wall) {
+      // the observer sees the state after this commit, on the calling thread,
+      // while later iterations run on the device (reduce.cpp:406-423)
+      I.hs.commit(s, r);
+      TraceRow row;
+      row.iteration = ++iteration;
+      row.s = s;
+      row.r = r;
+      row.smice = smice;
+      row.max_err.assign(me, me + I.L);
+      row.supernode_count = int(I.hs.supernodes.size());
+      row.candidate_count = c;
+      row.wall_ms = wall;
+      out.total_candidates += c;
+      obs(I.hs, row);
+      out.trace.push_back(std::move(row));
+    };
+    I.run_device_loop(ts, tr, tc, tsm, tme, tms, live ? &deliver : nullptr);
+    if (live) ts.clear();
     for (size_t i = 0; i < ts.size(); ++i) {
       I.hs.commit(ts[i], tr[i]);
       TraceRow row;

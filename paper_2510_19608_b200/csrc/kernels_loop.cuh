@@ -71,6 +71,13 @@ struct LoopArgs {
   cudaGraphConditionalHandle scond;  // switch over the scorer's row split (score1<1|2|4>)
   int use_scond;
   unsigned long long* tdbg;  // optional timeline [iter][8]: pick start/end, enum start/end
+  // live trace (observer delivery while the graph runs): rows mirrored into
+  // mapped host memory, then the published row count (null: off)
+  volatile int* live_count;
+  int* live_src;              // [cap][3]: s, r, candidate count
+  double* live_smice;         // [cap]
+  double* live_me;            // [cap][L]
+  unsigned long long* live_t; // [cap] globaltimer at commit
 };
 
 constexpr unsigned kPadEntry = 7u;  // rho 0, first, phase 3 (inert row)
@@ -173,7 +180,11 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   }
   const int ns = st->ns;
   if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 2] = globaltimer();
-  if (st->iter == 0 && tid == 0) a.tr_t[a.cap] = globaltimer();  // loop start: iteration 1's wall_ms
+  if (st->iter == 0 && tid == 0) {  // loop start: iteration 1's wall_ms
+    const unsigned long long t = globaltimer();
+    a.tr_t[a.cap] = t;
+    if (a.live_count) *reinterpret_cast<volatile unsigned long long*>(a.live_count + 2) = t;
+  }
 #ifdef ENUM_TIMING
   long long et[9];
 #endif
@@ -612,8 +623,18 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
       a.tr_smice[it] = bs;
       a.tr_t[it] = globaltimer();
     }
-    for (int l = tid; l < L; l += kLoopThreads)
-      a.tr_me[size_t(it) * L + l] = a.ldc > 0 ? a.pmaxerr[size_t(l) * a.ldc + bi] : a.pmaxerr[size_t(bi) * L + l];
+    for (int l = tid; l < L; l += kLoopThreads) {
+      const double me = a.ldc > 0 ? a.pmaxerr[size_t(l) * a.ldc + bi] : a.pmaxerr[size_t(bi) * L + l];
+      a.tr_me[size_t(it) * L + l] = me;
+      if (a.live_count) a.live_me[size_t(it) * L + l] = me;
+    }
+    if (a.live_count && tid == 0) {
+      a.live_src[3 * it] = s;
+      a.live_src[3 * it + 1] = r;
+      a.live_src[3 * it + 2] = C;
+      a.live_smice[it] = bs;
+      a.live_t[it] = globaltimer();
+    }
   }
   // i_agg[s] += i_agg[r], i_agg[r] = 0 (reduce.cpp:336-343); bounds merge
   const unsigned ms = a.mask[s], mr = a.mask[r];
@@ -659,6 +680,12 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
     if (a.has_target && double(a.n - (ns - 1)) / double(a.n) >= a.target) st->done = 1;
     if (it + 1 >= a.cap) st->done = 1;
     if (a.tdbg) a.tdbg[size_t(it) * kTdbg + 1] = globaltimer();
+    if (a.live_count && it < a.cap) {
+      // every thread's row stores precede the barriers above; make them
+      // visible to the host before the count that publishes the row
+      __threadfence_system();
+      *a.live_count = it + 1;
+    }
   }
 }
 

@@ -344,3 +344,44 @@ def test_scorer_row_split_bitwise(S, case, tag, e_bar, monkeypatch, tmp_path):
     out = tmp_path / "r.json"
     res.write_reduced_json(str(out))
     assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
+
+
+def test_cpp_engine_cache(tmp_path):
+    """kronred::run_reduction reuses its engine across calls on networks of the
+    same structure (tests/cpp/test_engine_cache.cpp): identical bits on a
+    repeated call, a fresh engine's bits with new values, no false hit on
+    another network."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2510_19608_b200" / "_lib"
+    kr.lib()
+    exe = tmp_path / "test_engine_cache"
+    subprocess.run(["g++", "-std=c++20", "-O2", f"-I{root / 'include'}", str(root / "tests" / "cpp" / "test_engine_cache.cpp"),
+                    f"-L{lib}", "-lkronred_b200", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    p = subprocess.run([str(exe), str(path("c2", "net.json")), str(path("c2", "scen.csv")), str(path("c1", "net.json")),
+                        str(path("c1", "scen.csv")), "3e-3"], capture_output=True, text=True)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "failures 0" in p.stdout
+    print(p.stdout)
+
+
+def test_observer_is_live():
+    """The observer runs while the device loop is still iterating (rows are
+    published through mapped host memory as they are committed), in commit
+    order, with the reference's rows (reduce.cpp:406-423); KRONRED_OBSERVER=
+    replay restores post-hoc delivery."""
+    import time
+    ctx = kr.Context(host("c2"))
+    cfg = kr.ReductionConfig(e_bar=3e-3)
+    ctx.run_reduction(cfg, observer=lambda row: None)  # graph instantiation
+    seen = []
+    t0 = time.perf_counter()
+    res = ctx.run_reduction(cfg, observer=lambda row: seen.append((time.perf_counter(), row.iteration, row.s, row.r)))
+    t1 = time.perf_counter()
+    assert [x[1] for x in seen] == list(range(1, len(res.trace) + 1))
+    assert [(s, r) for _, _, s, r in seen] == [(t.s, t.r) for t in res.trace]
+    assert_trace(res, "c2", "mag_3e-3")
+    # the first half of the rows arrive before the run is 3/4 done
+    mid = seen[len(seen) // 2][0]
+    assert mid - t0 < 0.75 * (t1 - t0), (mid - t0, t1 - t0)
