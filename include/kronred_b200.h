@@ -214,6 +214,13 @@ double krg_result_device_ms(const krg_result* res);
 /* Byte-compatible writers (io.cpp:216-265 and io.cpp:338-359). */
 int krg_result_write_reduced_json(const krg_result* res, const char* path);
 int krg_result_write_trace_csv(const krg_result* res, const char* path, int32_t zero_wall);
+/* Validation report of a reduced model against the context's network and
+ * scenario library: per-scenario max errors (model_max_errors on the device)
+ * and a `bins`-bin histogram, as the CSV the reference writes
+ * (make_validate_report + write_validate_report, io.cpp:385-416). Writes up
+ * to cap-1 bytes plus NUL into out (may be null); returns the full length, or
+ * minus a KRG_E_* status. */
+int64_t krg_validate_report(krg_ctx* ctx, const krg_result* res, int32_t bins, char* out, int64_t cap);
 void krg_result_free(krg_result* res);
 
 #ifdef __cplusplus

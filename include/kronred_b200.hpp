@@ -243,6 +243,17 @@ ReducedModel radialize(const ReducedModel& model, const Network& original, const
 std::vector<double> model_max_errors(const ReducedModel& model, const Network& net,
                                      const ScenarioLibrary& lib);
 
+// --- validation report (io.hpp:62-71, io.cpp:385-416) ----------------------
+struct ValidateReport {
+  std::vector<std::string> scenario_ids;
+  std::vector<double> max_err;    // per scenario (model_max_errors, on the device)
+  std::vector<double> bin_edges;  // histogram over max_err, size bins+1
+  std::vector<int> bin_counts;    // size bins
+};
+ValidateReport make_validate_report(const ReducedModel& model, const Network& net, const ScenarioLibrary& lib,
+                                    int bins = 20);
+void write_validate_report(const ValidateReport& rep, const std::string& path);
+
 // --- writers (io.cpp:216-359) ------------------------------------------------
 std::string format_double(double v);
 std::string reduced_json_string(const ReducedModel& model);

@@ -12,7 +12,7 @@
 //          reproduces the generated library bit-for-bit (scenario.cpp:39-50).
 //   reduce --net f --scen f [--e-bar E] [--objective mag|complex] [--target T]
 //          [--workers W] [--radialize] [--reduced out.json] [--trace out.csv]
-//          [--trace-hex out.txt]
+//          [--trace-hex out.txt] [--validate report.csv [--bins k]]
 //          Runs kronred::run_reduction (reduce.cpp:349-451) and prints one JSON
 //          summary line (wall, iterations, candidates, cand/s).
 //   scores --net f --scen f [--e-bar E] [--objective ...] --iters K --out f
@@ -171,6 +171,8 @@ int cmd_reduce(const std::map<std::string, std::string>& a) {
   }
   const double wall = std::chrono::duration<double>(t1 - t0).count();
   if (a.count("reduced")) write_reduced_json(model, gets(a, "reduced", ""));
+  if (a.count("validate"))  // io.cpp:385-416 on the model just reduced
+    write_validate_report(make_validate_report(model, net, lib, int(getl(a, "bins", 20))), gets(a, "validate", ""));
   if (a.count("trace")) {
     // wall_ms is nondeterministic; zero it so the file is a stable golden
     std::vector<TraceRow> tr = res.trace;

@@ -135,6 +135,7 @@ _SIGS = [
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("krg_fp64_probe", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
     ("krg_result_device_ms", C.c_double, [C.c_void_p]),
+    ("krg_validate_report", C.c_int64, [C.c_void_p, C.c_void_p, C.c_int32, C.c_char_p, C.c_int64]),
     ("krg_selftest_sqrt", C.c_int, [C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_int64)]),
 ]
 
@@ -569,6 +570,15 @@ class Context:
         out = np.zeros(nphi * nphi * 2)
         _check(lib().krg_zcols(self._h, _p(out, C.c_double), out.size))
         return out.view(np.complex128).reshape(nphi, nphi)  # [column][row]
+
+    def validate_report(self, result: "Result", bins: int = 20) -> str:
+        """make_validate_report + write_validate_report (io.cpp:385-416) as a string."""
+        n = lib().krg_validate_report(self._h, result._h, bins, None, 0)
+        if n < 0:
+            _check(int(-n))
+        buf = C.create_string_buffer(int(n) + 1)
+        _check(0 if lib().krg_validate_report(self._h, result._h, bins, buf, n + 1) >= 0 else 1)
+        return buf.value.decode()
 
     def kron_reduce(self, reduce: Sequence[int]) -> Result:
         red = np.ascontiguousarray(sorted(set(int(x) for x in reduce)) or [0], np.int32)

@@ -454,6 +454,17 @@ std::vector<double> model_max_errors(const ReducedModel& model, const Network& n
   return cached_engine(problem_from(net, &lib)).model_errors(model);
 }
 
+ValidateReport make_validate_report(const ReducedModel& model, const Network& net, const ScenarioLibrary& lib,
+                                    int bins) {
+  return validate_report(lib.ids(), model_max_errors(model, net, lib), bins);
+}
+
+void write_validate_report(const ValidateReport& rep, const std::string& path) {
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw Error("cannot write " + path);
+  f << validate_csv(rep);
+}
+
 void release_engine_cache() {
   t_engine_cache.eng.reset();
   t_engine_cache.key.clear();
@@ -846,6 +857,21 @@ int krg_result_write_reduced_json(const krg_result* r, const char* path) {
   write_reduced_json(r->d.model, path);
   return KRG_OK;
   KRG_CATCH
+}
+
+int64_t krg_validate_report(krg_ctx* ctx, const krg_result* res, int32_t bins, char* out, int64_t cap) {
+  try {
+    const std::string csv =
+        validate_csv(validate_report(res->d.model.scenario_ids, ctx->eng->model_errors(res->d.model), bins));
+    if (out && cap > 0) {
+      const size_t k = std::min(size_t(cap - 1), csv.size());
+      std::memcpy(out, csv.data(), k);
+      out[k] = '\0';
+    }
+    return int64_t(csv.size());
+  } catch (...) {
+    return -int64_t(status_from_current_exception());
+  }
 }
 
 int krg_result_write_trace_csv(const krg_result* r, const char* path, int32_t zero_wall) {

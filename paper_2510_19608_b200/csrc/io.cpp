@@ -1,6 +1,7 @@
 // Result writers, byte-compatible with the reference's reduced-model JSON
 // (io.cpp:216-265) and trace CSV (io.cpp:338-359) so downstream consumers of
 // `kronred reduce --out reduced.json --trace trace.csv` see identical files.
+#include <algorithm>
 #include <cstdio>
 #include <fstream>
 #include <sstream>
@@ -112,6 +113,34 @@ std::string trace_csv(const std::vector<TraceRow>& trace, const std::vector<std:
   o << ",";
   if (!trace.empty()) o << trace.back().supernode_count;
   o << ",,\n";
+  return o.str();
+}
+
+// validation report: histogram of per-scenario errors (io.cpp:385-416)
+ValidateReport validate_report(const std::vector<std::string>& ids, const std::vector<double>& max_err, int bins) {
+  ValidateReport rep;
+  rep.scenario_ids = ids;
+  rep.max_err = max_err;
+  if (bins < 1) bins = 1;
+  double top = 0;
+  for (const double e : max_err) top = std::max(top, e);
+  if (top <= 0) top = 1e-12;
+  top *= 1.0 + 1e-12;  // the largest error falls inside the last bin
+  rep.bin_edges.resize(size_t(bins) + 1);
+  for (int b = 0; b <= bins; ++b) rep.bin_edges[size_t(b)] = top * double(b) / double(bins);
+  rep.bin_counts.assign(size_t(bins), 0);
+  for (const double e : max_err) ++rep.bin_counts[size_t(std::clamp(int(e / top * bins), 0, bins - 1))];
+  return rep;
+}
+
+std::string validate_csv(const ValidateReport& rep) {
+  std::ostringstream o;
+  o << "record,scenario_id,max_err,bin_lo,bin_hi,count\n";
+  for (size_t i = 0; i < rep.scenario_ids.size(); ++i)
+    o << "scenario," << rep.scenario_ids[i] << "," << format_double(rep.max_err[i]) << ",,,\n";
+  for (size_t b = 0; b < rep.bin_counts.size(); ++b)
+    o << "hist,,," << format_double(rep.bin_edges[b]) << "," << format_double(rep.bin_edges[b + 1]) << ","
+      << rep.bin_counts[b] << "\n";
   return o.str();
 }
 

@@ -177,6 +177,9 @@ std::string trace_csv(const std::vector<TraceRow>& trace, const std::vector<std:
                       const std::vector<double>& final_max_err,
                       const std::vector<std::string>& comments);
 
+ValidateReport validate_report(const std::vector<std::string>& ids, const std::vector<double>& max_err, int bins);
+std::string validate_csv(const ValidateReport& rep);
+
 // radialization host helpers
 ReducedModel radialize_host(const ReducedModel& model, const Network& original,
                             const std::function<void(const std::vector<int>&, ReducedModel&)>& kron,

@@ -173,6 +173,28 @@ def long(which: list[str]) -> None:
             raise SystemExit(f"unknown long step {w}")
 
 
+def traces() -> None:
+    """Trace CSV (io.cpp:338-359, wall_ms zeroed) and validate report
+    (io.cpp:385-416, 20 bins) bytes of reference runs, for the writers'
+    byte-level parity (run separately: `make_golden.py traces`)."""
+    jobs = [("c1", "mag_1e-3", "scen.csv", ["--e-bar", "1e-3"], False),
+            ("c1", "rad_1e-2_t06", "scen.csv", ["--e-bar", "1e-2", "--target", "0.6"], True),
+            ("m40", "mag_1e-3", "scen.csv", ["--e-bar", "1e-3"], False),
+            ("pq30", "pq_1e-3", "scen_pq.csv", ["--e-bar", "1e-3"], False),
+            ("c2", "mag_3e-3", "scen.csv", ["--e-bar", "3e-3", "--workers", "0"], False)]
+    for case, tag, scen, flags, rad in jobs:
+        d = HERE / case
+        net = _inflate(case, "net.json") if (d / "net.json.gz").exists() else d / "net.json"
+        sc = _inflate(case, scen) if (d / (scen + ".gz")).exists() else d / scen
+        args = ["reduce", "--net", str(net), "--scen", str(sc), *flags, "--trace", str(d / f"tracecsv_{tag}.csv"),
+                "--validate", str(d / f"validate_{tag}.csv"), "--bins", "20"]
+        if rad:
+            args.append("--radialize")
+        run(*args)
+        if case == "c2":
+            gz(d / f"tracecsv_{tag}.csv")
+
+
 def naive() -> None:
     """use_delta = false (eval_full_solve, reduce.cpp:132-167) on the small
     feeders: its full solves round differently from the delta path."""
@@ -190,6 +212,9 @@ def main() -> None:
         return
     if sys.argv[1:2] == ["long"]:
         long(sys.argv[2:] or ["h2k", "c3", "c4L24", "c5", "c4"])
+        return
+    if sys.argv[1:] == ["traces"]:
+        traces()
         return
     if sys.argv[1:] == ["naive"]:
         naive()

@@ -385,3 +385,24 @@ def test_observer_is_live():
     # the first half of the rows arrive before the run is 3/4 done
     mid = seen[len(seen) // 2][0]
     assert mid - t0 < 0.75 * (t1 - t0), (mid - t0, t1 - t0)
+
+
+@pytest.mark.parametrize("case,tag,scen,flags,rad", [
+    ("c1", "mag_1e-3", "scen.csv", ["--e-bar", "1e-3"], False),
+    ("c1", "rad_1e-2_t06", "scen.csv", ["--e-bar", "1e-2", "--target", "0.6"], True),
+    ("m40", "mag_1e-3", "scen.csv", ["--e-bar", "1e-3"], False),
+    ("pq30", "pq_1e-3", "scen_pq.csv", ["--e-bar", "1e-3"], False),
+    ("c2", "mag_3e-3", "scen.csv", ["--e-bar", "3e-3"], False),
+])
+def test_trace_csv_and_validate_report_bytes(case, tag, scen, flags, rad, tmp_path):
+    """write_trace_csv (io.cpp:338-359; wall_ms zeroed as in the golden) and the
+    validate report (make_validate_report + write_validate_report,
+    io.cpp:385-416, 20 bins) are byte-identical to the reference's files."""
+    ctx = kr.Context(host(case, scen))
+    res = ctx.run_reduction(cfg_from_flags(flags))
+    if rad:
+        ctx.radialize(res, with_errors=True)
+    out = tmp_path / "trace.csv"
+    res.write_trace_csv(str(out), zero_wall=True)
+    assert out.read_text() == path(case, f"tracecsv_{tag}.csv").read_text()
+    assert ctx.validate_report(res, 20) == path(case, f"validate_{tag}.csv").read_text()
