@@ -148,6 +148,19 @@ int krg_selftest_sqrt(int64_t n, double lo, double hi, int64_t* mismatches);
 int krg_selftest_cdiv(const double* in, int32_t N, double* out, int32_t on_device);
 int krg_set_exchange(krg_ctx* ctx, int32_t rank, int32_t world, krg_exchange_fn fn,
                      void* user);
+/* Multi-GPU inside the device loop (the reference's worker split,
+ * parallel.cpp:11-34, across GPUs): one context per rank and GPU, all built
+ * from the same problem. Rank 0 makes an id with krg_nccl_unique_id and hands
+ * it to every rank (any side channel); every rank then calls krg_set_comm
+ * (collective: an NCCL communicator, a symmetric window of per-rank records,
+ * a device communicator with one LSA barrier). Each iteration every rank
+ * scores its contiguous range of the candidate list and the pick kernel
+ * exchanges one {smice, index, max_err[L]} record per rank through the window
+ * (NVLink peer stores + LSA barrier) inside the loop graph; all ranks commit
+ * the same candidate. */
+#define KRG_NCCL_ID_BYTES 128
+int krg_nccl_unique_id(uint8_t* out /* KRG_NCCL_ID_BYTES */);
+int krg_set_comm(krg_ctx* ctx, int32_t rank, int32_t world, const uint8_t* unique_id);
 /* Number of kernels this context has launched so far. */
 int64_t krg_launch_count(const krg_ctx* ctx);
 /* Per-kernel CUDA-event timing on the launching stream (bench/roofline only):

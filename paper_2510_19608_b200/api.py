@@ -97,6 +97,8 @@ _SIGS = [
     ("krg_destroy", None, [C.c_void_p]),
     ("krg_selftest_cdiv", C.c_int, [C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double), C.c_int32]),
     ("krg_set_exchange", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, EXCHANGE_FN, C.c_void_p]),
+    ("krg_nccl_unique_id", C.c_int, [C.c_char_p]),
+    ("krg_set_comm", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p]),
     ("krg_launch_count", C.c_int64, [C.c_void_p]),
     ("krg_scenario_voltages", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("krg_run_reduction", C.c_int, [C.c_void_p, C.POINTER(KrgConfig), OBSERVER_FN, C.c_void_p,
@@ -297,6 +299,14 @@ def merge_best(smice: Sequence[float], index: Sequence[int]) -> int:
     s = _f64(smice)
     i = np.ascontiguousarray(index, np.int64)
     return int(lib().krg_merge_best(_p(s, C.c_double), _p(i, C.c_int64), len(s)))
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 makes it, every rank passes it to
+    Context.set_comm)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().krg_nccl_unique_id(buf))
+    return buf.raw
 
 
 def fp64_probe(device: int = -1) -> float:
@@ -507,6 +517,13 @@ class Context:
 
         self._cb = EXCHANGE_FN(_cb)
         _check(lib().krg_set_exchange(self._h, rank, world, self._cb, None))
+
+    def set_comm(self, rank: int, world: int, unique_id: bytes) -> None:
+        """In-graph multi-GPU exchange (krg_set_comm): collective over the
+        `world` ranks, each with its own context on its own GPU."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        _check(lib().krg_set_comm(self._h, rank, world, unique_id))
 
     def run_reduction(self, cfg: ReductionConfig, observer: Optional[Callable[[TraceRow], None]] = None) -> Result:
         """run_reduction (reduce.cpp:349-451)."""

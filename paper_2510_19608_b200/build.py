@@ -16,7 +16,11 @@ LIB = OUT / "libkronred_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+# NCCL 2.28 (host + device API: symmetric windows, LSA barriers) for the
+# in-graph multi-GPU min-loc exchange; the torch-bundled build of this image
+NCCL = Path(os.environ.get("KRONRED_NCCL", "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"))
+COMMON = ["-O3", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{NCCL / 'include'}"]
+NCCL_LINK = [f"-L{NCCL / 'lib'}", "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", str(NCCL / "lib")]
 NVFLAGS = COMMON + ARCH + ["-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
                            "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 CXXFLAGS = COMMON + ["-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", "-I/usr/local/cuda/include"]
@@ -58,7 +62,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         logs = list(ex.map(_run, jobs))
     (OUT / "ptxas.log").write_text("\n".join(l for l in logs if l))
     tmp = LIB.with_suffix(".so.tmp")
-    _run([NVCC, "-shared", *ARCH, "-o", str(tmp), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    _run([NVCC, "-shared", *ARCH, "-o", str(tmp), *map(str, objs), *NCCL_LINK, "-lcudart_static", "-lrt", "-ldl",
+          "-lpthread"])
     os.replace(tmp, LIB)
     if verbose:
         print(f"built {LIB}")
@@ -80,7 +85,8 @@ def build_variant(out_dir: Path, defines: list[str]) -> Path:
             obj = OUT / (src.name + ".o")
         objs.append(obj)
     lib = out_dir / LIB.name
-    _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+    _run([NVCC, "-shared", *ARCH, "-o", str(lib), *map(str, objs), *NCCL_LINK, "-lcudart_static", "-lrt", "-ldl",
+          "-lpthread"])
     return lib
 
 

@@ -644,6 +644,13 @@ int krg_set_exchange(krg_ctx* ctx, int32_t rank, int32_t world, krg_exchange_fn 
   KRG_CATCH
 }
 
+int krg_set_comm(krg_ctx* ctx, int32_t rank, int32_t world, const uint8_t* unique_id) {
+  KRG_TRY
+  ctx->eng->set_comm(rank, world, unique_id);
+  return KRG_OK;
+  KRG_CATCH
+}
+
 int64_t krg_launch_count(const krg_ctx* ctx) { return ctx ? ctx->eng->launches() : 0; }
 
 int krg_set_profile(krg_ctx* ctx, int32_t on) {

@@ -23,6 +23,8 @@
 // Exactness: see kr_device.cuh. Every decision is bit-identical to the
 // reference CPU program (tests/test_gpu_parity.py).
 #include <cuda_runtime.h>
+#include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 #include <chrono>
@@ -330,6 +332,44 @@ struct Engine::Impl {
   int rank = 0, world = 1;
   krg_exchange_fn xfn = nullptr;
   void* xuser = nullptr;
+  // in-graph exchange: NCCL communicator, symmetric window of per-rank records
+  // (2 parities x world x rec_bytes), device communicator with one LSA barrier
+  ncclComm_t comm = nullptr;
+  ncclWindow_t win = nullptr;
+  void* winbuf = nullptr;
+  ncclDevComm dcomm{};
+  int rec_bytes = 0, xemul = 1;
+  static void nk(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error(std::string("NCCL error in ") + what + ": " + ncclGetErrorString(r));
+  }
+  void set_comm(int rk, int ws, const ncclUniqueId& id) {
+    if (ws < 1 || rk < 0 || rk >= ws) throw ConfigError("bad rank/world");
+    free_comm();
+    CK(cudaSetDevice(device));
+    nk(ncclCommInitRank(&comm, ws, id, rk), "ncclCommInitRank");
+    rec_bytes = (24 + 8 * std::max(L, 1) + 15) & ~15;
+    // test aid: a one-rank communicator playing KRONRED_XCH_EMULATE ranks
+    xemul = ws == 1 && std::getenv("KRONRED_XCH_EMULATE") ? std::max(1, std::atoi(std::getenv("KRONRED_XCH_EMULATE"))) : 1;
+    const size_t bytes = (size_t(2) * std::max(ws, xemul) * rec_bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) /
+                         NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    nk(ncclMemAlloc(&winbuf, bytes), "ncclMemAlloc");
+    nk(ncclCommWindowRegister(comm, winbuf, bytes, &win, NCCL_WIN_COLL_SYMMETRIC), "ncclCommWindowRegister");
+    ncclDevCommRequirements req{};
+    req.lsaBarrierCount = 1;
+    nk(ncclDevCommCreate(comm, &req, &dcomm), "ncclDevCommCreate");
+    rank = rk;
+    world = ws;
+  }
+  void free_comm() {
+    if (!comm) return;
+    ncclDevCommDestroy(comm, &dcomm);
+    ncclCommWindowDeregister(comm, win);
+    ncclMemFree(winbuf);
+    ncclCommDestroy(comm);
+    comm = nullptr;
+    win = nullptr;
+    winbuf = nullptr;
+  }
   // loop state
   ReductionConfig cfg;
   HostState hs;
@@ -392,6 +432,7 @@ struct Engine::Impl {
   const void* loop_key_bufs[kLoopKeyBufs] = {};
   int loop_key_L = -1;
   bool loop_key_live = false;
+  ncclComm_t loop_key_comm = nullptr;
   DBuf<unsigned long long> d_tdbg;
   bool loop_trace = std::getenv("KRONRED_LOOP_TRACE") != nullptr;
   bool force_host_loop = std::getenv("KRONRED_LOOP") != nullptr && std::string(std::getenv("KRONRED_LOOP")) == "host";
@@ -890,7 +931,7 @@ struct Engine::Impl {
       e.pivot_floor = floor;
       e.fail = d.fail.p;
       e.fail_pivot = d.fail_pivot.p;
-      elim_factor_kernel<<<1, 1024, 0, stream>>>(e);
+      elim_factor_kernel<<<1, ELIM_THREADS, 0, stream>>>(e);
       launched();
       CK(cudaGetLastError());
     }
@@ -1109,6 +1150,8 @@ struct Engine::Impl {
   // the voltages are not given, scenario.cpp:39-50).
   void load_scenarios(const std::vector<std::string>& ids, const std::vector<double>& inj,
                       const std::vector<double>& volt) {
+    if (comm && (24 + 8 * int(ids.size()) + 15) / 16 * 16 > rec_bytes)
+      throw ConfigError("set_comm before loading a library with more scenarios (exchange records are sized by L)");
     L = int(ids.size());
     prob.L = L;
     prob.scenario_ids = ids;
@@ -1147,6 +1190,7 @@ struct Engine::Impl {
   }
 
   ~Impl() {
+    free_comm();
     if (ev_a) {
       cudaEventDestroy(ev_a);
       cudaEventDestroy(ev_b);
@@ -1511,7 +1555,7 @@ struct Engine::Impl {
   size_t enum_smem() const { return (enum_kcap() + 2 * prob.net.branches.size() + 1) * sizeof(unsigned); }
 
   bool device_loop_ok(const ReductionConfig& c) const {
-    return !force_host_loop && c.use_delta && c.objective == Objective::magnitude && world == 1 && !profile &&
+    return !force_host_loop && c.use_delta && c.objective == Objective::magnitude && (world == 1 || comm) && !profile &&
            full.bW > 0 && n <= 65535 && enum_smem() + 24 * 1024 <= size_t(optin_smem);
   }
 
@@ -1534,6 +1578,13 @@ struct Engine::Impl {
     a.fill = s3_fill();
     a.force_s = s3_force;
     a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
+    a.rank = comm ? rank : 0;
+    a.world = comm ? world : 1;
+    a.xch = comm ? 1 : 0;
+    a.dcomm = dcomm;
+    a.win = win;
+    a.rec_bytes = rec_bytes;
+    a.xemul = (comm && world == 1) ? xemul : 1;
     a.has_target = cfg.target_reduction ? 1 : 0;
     a.target = cfg.target_reduction ? *cfg.target_reduction : 0.0;
     a.br_from = d_brf.p;
@@ -1682,7 +1733,7 @@ struct Engine::Impl {
                                       d_Z.p,    d_psmice.p, d_grpdone.p, d_loopst.p, d_trme.p, d_sup.p};
     const bool key_ok = loop_exec && loop_key_ebar == cfg.e_bar && loop_key_has == la.has_target &&
                         loop_key_target == la.target && loop_key_trace == loop_trace && loop_key_L == L &&
-                        loop_key_live == (la.live_count != nullptr) &&
+                        loop_key_live == (la.live_count != nullptr) && loop_key_comm == comm &&
                         std::equal(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     if (!key_ok) {
       if (loop_exec) CK(cudaGraphExecDestroy(loop_exec));
@@ -1781,6 +1832,7 @@ struct Engine::Impl {
       loop_key_trace = loop_trace;
       loop_key_L = L;
       loop_key_live = la.live_count != nullptr;
+      loop_key_comm = comm;
       std::copy(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     }
     // the whole loop: one graph launch (a loop that is already done runs one
@@ -1935,6 +1987,12 @@ KernelStats Engine::stats(int which) const {
 }
 const Problem& Engine::problem() const { return impl_->prob; }
 std::int64_t Engine::launches() const { return impl_->launches; }
+
+void Engine::set_comm(int rank, int world, const void* unique_id) {
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof id);
+  impl_->set_comm(rank, world, id);
+}
 
 void Engine::set_exchange(int rank, int world, krg_exchange_fn fn, void* user) {
   if (world < 1 || rank < 0 || rank >= world) throw ConfigError("bad rank/world");
@@ -2399,6 +2457,19 @@ void Engine::radialize(ReducedModel& model, bool with_errors) {
     return this->model_errors(m);
   };
   model = radialize_host(model, impl_->prob.net, kr, with_errors ? &errs : nullptr);
+}
+
+extern "C" int krg_nccl_unique_id(uint8_t* out) {
+  try {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw Error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == KRG_NCCL_ID_BYTES, "NCCL unique id size");
+    std::memcpy(out, &id, sizeof id);
+    return KRG_OK;
+  } catch (...) {
+    return status_from_current_exception();
+  }
 }
 
 // measured unfused FP64 rate (GFLOP/s, DMUL+DADD counted as 2) on `device`

@@ -46,6 +46,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 struct LoopState {
   int done, iter, ns, C, R, err;
   int S;             // scorer lanes per (candidate, scenario) pair this iteration
+  int c0, Cl;        // this rank's candidate range [c0, c0 + Cl) of the C (lexicographic); c0 = 0, Cl = C on one GPU
   int last_s, last_r;  // the last committed candidate (incremental base refresh)
   int grp_start[4];  // candidate offset of each |phi(r)| group (index 1..3)
   int grp_cta[4];    // first CTA of each group; grp_cta[3] = CTAs in use

@@ -52,32 +52,33 @@ __device__ __forceinline__ void matmul(const C2 a[9], const C2 b[9], C2 r[9]) {
 
 __device__ __forceinline__ double cabs_dev(C2 z) { return hypot(z.x, z.y); }
 
-// masked_inverse (complex3.cpp:9-61). Pivot magnitudes use hypot (glibc cabs
-// on the host); they only select pivots / gate singularity.
-__device__ bool masked_inverse(const C2 in[9], unsigned mask, C2 out[9], double tol, double& smallest) {
+// masked_inverse (complex3.cpp:9-61): Gauss-Jordan with partial pivoting on
+// the K x K present-phase submatrix, compiled per K so the work arrays stay in
+// registers (the row swap is a predicated exchange with every candidate row).
+// Pivot magnitudes use hypot (glibc cabs on the host); they only select
+// pivots / gate singularity. Divisions are the __divdc3 replica.
+template <unsigned MASK>
+__device__ __forceinline__ bool masked_inverse_k(const C2 in[9], C2 out[9], double tol, double& smallest) {
+  constexpr int K = int((MASK & 1u) + ((MASK >> 1) & 1u) + ((MASK >> 2) & 1u));
+  // present phases, ascending (compile-time: every index below is static)
+  constexpr int i0 = (MASK & 1u) ? 0 : ((MASK & 2u) ? 1 : 2);
+  constexpr int i1 = K < 2 ? 0 : ((MASK & 1u) ? ((MASK & 2u) ? 1 : 2) : 2);
+  constexpr int idx[3] = {i0, i1, 2};
+  C2 a[K][K], inv[K][K];
 #pragma unroll
-  for (int e = 0; e < 9; ++e) out[e] = {0.0, 0.0};
-  int idx[3];
-  int k = 0;
-  for (int p = 0; p < 3; ++p)
-    if ((mask >> p) & 1u) idx[k++] = p;
-  smallest = 0.0;
-  if (k == 0) return true;
-  C2 a[3][3], inv[3][3];
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) {
-      a[i][j] = {0.0, 0.0};
-      inv[i][j] = {0.0, 0.0};
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      a[i][j] = in[idx[i] * 3 + idx[j]];
+      inv[i][j] = i == j ? C2{1.0, 0.0} : C2{0.0, 0.0};
     }
-  for (int i = 0; i < k; ++i) {
-    inv[i][i] = {1.0, 0.0};
-    for (int j = 0; j < k; ++j) a[i][j] = in[idx[i] * 3 + idx[j]];
-  }
   smallest = __longlong_as_double(0x7ff0000000000000LL);
-  for (int col = 0; col < k; ++col) {
+#pragma unroll
+  for (int col = 0; col < K; ++col) {
     int piv = col;
     double best = cabs_dev(a[col][col]);
-    for (int r = col + 1; r < k; ++r) {
+#pragma unroll
+    for (int r = col + 1; r < K; ++r) {
       const double m = cabs_dev(a[r][col]);
       if (m > best) {
         best = m;
@@ -86,33 +87,57 @@ __device__ bool masked_inverse(const C2 in[9], unsigned mask, C2 out[9], double 
     }
     smallest = fmin(smallest, best);
     if (best <= tol) return false;
-    if (piv != col)
-      for (int j = 0; j < 3; ++j) {
-        C2 t = a[piv][j];
-        a[piv][j] = a[col][j];
-        a[col][j] = t;
-        t = inv[piv][j];
-        inv[piv][j] = inv[col][j];
-        inv[col][j] = t;
-      }
+#pragma unroll
+    for (int r = col + 1; r < K; ++r)
+      if (piv == r)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          C2 t = a[r][j];
+          a[r][j] = a[col][j];
+          a[col][j] = t;
+          t = inv[r][j];
+          inv[r][j] = inv[col][j];
+          inv[col][j] = t;
+        }
     const C2 d = a[col][col];
-    for (int j = 0; j < k; ++j) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
       a[col][j] = dev::cdiv(a[col][j], d);
       inv[col][j] = dev::cdiv(inv[col][j], d);
     }
-    for (int r = 0; r < k; ++r) {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
       if (r == col) continue;
       const C2 f = a[r][col];
       if (dev::cis0(f)) continue;
-      for (int j = 0; j < k; ++j) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
         a[r][j] = dev::csub(a[r][j], dev::cmul(f, a[col][j]));
         inv[r][j] = dev::csub(inv[r][j], dev::cmul(f, inv[col][j]));
       }
     }
   }
-  for (int i = 0; i < k; ++i)
-    for (int j = 0; j < k; ++j) out[idx[i] * 3 + idx[j]] = inv[i][j];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) out[idx[i] * 3 + idx[j]] = inv[i][j];
   return true;
+}
+
+__device__ bool masked_inverse(const C2 in[9], unsigned mask, C2 out[9], double tol, double& smallest) {
+#pragma unroll
+  for (int e = 0; e < 9; ++e) out[e] = {0.0, 0.0};
+  smallest = 0.0;
+  switch (mask & 7u) {
+    case 1: return masked_inverse_k<1>(in, out, tol, smallest);
+    case 2: return masked_inverse_k<2>(in, out, tol, smallest);
+    case 3: return masked_inverse_k<3>(in, out, tol, smallest);
+    case 4: return masked_inverse_k<4>(in, out, tol, smallest);
+    case 5: return masked_inverse_k<5>(in, out, tol, smallest);
+    case 6: return masked_inverse_k<6>(in, out, tol, smallest);
+    case 7: return masked_inverse_k<7>(in, out, tol, smallest);
+    default: return true;  // nothing present: the pseudo-inverse of 0 is 0
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -134,7 +159,10 @@ struct ElimDev {
   double* fail_pivot;
 };
 
-__global__ void __launch_bounds__(1024) elim_factor_kernel(ElimDev e) {
+#ifndef ELIM_THREADS  // threads of the single-CTA level executor (register budget 65536 / ELIM_THREADS)
+#define ELIM_THREADS 256
+#endif
+__global__ void __launch_bounds__(ELIM_THREADS) elim_factor_kernel(ElimDev e) {
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int lev = 0; lev < e.nlevels; ++lev) {
     // A1: structural pseudo-inverse of every pivot at this level

@@ -73,6 +73,15 @@ struct LoopArgs {
   unsigned long long* tdbg;  // optional timeline [iter][8]: pick start/end, enum start/end
   // live trace (observer delivery while the graph runs): rows mirrored into
   // mapped host memory, then the published row count (null: off)
+  // multi-GPU (one rank per GPU): candidates of an iteration are split in
+  // contiguous ranges (parallel.cpp:21-29); the pick exchanges one record per
+  // rank through an NCCL symmetric window (NVLink peer stores) and an LSA
+  // barrier, then every rank commits the lexicographic minimum
+  int rank, world, xch;
+  ncclDevComm dcomm;
+  ncclWindow_t win;
+  int rec_bytes;              // per-rank record: {smice, index, key, pad, max_err[L]}
+  int xemul;                  // > 1: one GPU plays xemul ranks (test aid, KRONRED_XCH_EMULATE)
   volatile int* live_count;
   int* live_src;              // [cap][3]: s, r, candidate count
   double* live_smice;         // [cap]
@@ -431,8 +440,11 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   // totals first (packed 3 x 21-bit counters, block reduction), then per
   // round a warp-ballot rank, a scan of the 32 warp counts and running group
   // bases.
+  // this rank's contiguous range of the sorted list (parallel.cpp:21-29)
+  const int xbase = C / a.world, xextra = C % a.world;
+  const int c0 = a.rank * xbase + min(a.rank, xextra), Cl = xbase + (a.rank < xextra ? 1 : 0);
   unsigned long long mine = 0;
-  for (int i = tid; i < C; i += kLoopThreads) mine += 1ull << (21 * (__popc(a.mask[keys[i] & 0xffffu]) - 1));
+  for (int i = c0 + tid; i < c0 + Cl; i += kLoopThreads) mine += 1ull << (21 * (__popc(a.mask[keys[i] & 0xffffu]) - 1));
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
   if (lane == 0) gscan[warp] = mine;
   __syncthreads();
@@ -449,10 +461,10 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   __syncthreads();
   const int cnt1 = s_gbase[2], cnt2 = s_gbase[3] - s_gbase[2];
   const unsigned lane_lt = (1u << lane) - 1u;
-  for (int r0 = 0; r0 < C; r0 += kLoopThreads) {
-    const int i = r0 + tid;
+  for (int r0 = 0; r0 < Cl; r0 += kLoopThreads) {
+    const int i = c0 + r0 + tid;  // global (lexicographic) index
     int s = 0, r = 0, g = 0;
-    if (i < C) {
+    if (r0 + tid < Cl) {
       s = int(keys[i] >> 16);
       r = int(keys[i] & 0xffffu);
       g = __popc(a.mask[r]);
@@ -480,7 +492,7 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
       }
     }
     __syncthreads();
-    if (i < C) {
+    if (r0 + tid < Cl) {
       const unsigned bg = g == 1 ? b1 : (g == 2 ? b2 : b3);
       const int p = s_wcnt[warp][g] + __popc(bg & lane_lt);
       a.cand[p] = make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
@@ -506,13 +518,15 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     }
   }
   if (tid == 0) {
-    const int cnt3 = C - cnt1 - cnt2;
-    const int S = s3_lanes((long long)C * a.L, a.fill, a.force_s);
+    const int cnt3 = Cl - cnt1 - cnt2;
+    const int S = s3_lanes((long long)Cl * a.L, a.fill, a.force_s);
     const int gk1 = a.gk1[S == 1 ? 0 : (S == 2 ? 1 : 2)];
     const int Sm = gk1 > 0 ? a.s_multi : S;  // split of the |phi(r)| >= 2 groups
     const int cpc1 = gk1 > 0 ? gk1 : s3_cpc(a.G3, 1, S), cpc2 = s3_cpc(a.G3, 2, Sm), cpc3 = s3_cpc(a.G3, 3, Sm);
     st->S = S;
     st->C = C;
+    st->c0 = c0;
+    st->Cl = Cl;
     if (a.use_scond) cudaGraphSetConditional(a.scond, S == 1 ? 0u : (S == 2 ? 1u : 2u));
     st->grp_start[0] = 0;
     st->grp_start[1] = 0;
@@ -540,26 +554,16 @@ __device__ __forceinline__ bool loop_better(double s1, int i1, double s2, int i2
   return s1 < s2 || (s1 == s2 && i1 < i2);
 }
 
-__global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
-  __shared__ double ss[32];
-  __shared__ int si[32];
-  __shared__ unsigned sk[32];
-  __shared__ int s_pos;
-  griddep_wait();
-  LoopState* st = a.st;
-  if (st->done) return;
+// first minimum feasible SMICE over candidates [lo, hi) (reduce.cpp:397-404),
+// with its (s, r) key: thread strided scan, warp shuffles, then warp 0;
+// every thread returns the block's result
+__device__ __forceinline__ void pick_block_argmin(const LoopArgs& a, int lo, int hi, double* ss, int* si, unsigned* sk,
+                                                  double& bs, int& bi, unsigned& bk) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int C = st->C;
-  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 0] = globaltimer();
-  // the commit's first reads (super-node map and active list, which only this
-  // kernel writes) are issued ahead of the argmin
-  const int sup0 = tid < a.n ? a.sup[tid] : -1;
-  const int sn0 = tid < st->ns ? a.sn[tid] : -1;
-  // argmin with the candidate's (s, r) carried along (no dependent load after it)
-  double bs = __longlong_as_double(0x7ff0000000000000LL);
-  int bi = -1;
-  unsigned bk = 0u;
-  for (int c = tid; c < C; c += kLoopThreads) {
+  bs = __longlong_as_double(0x7ff0000000000000LL);
+  bi = -1;
+  bk = 0u;
+  for (int c = lo + tid; c < hi; c += kLoopThreads) {
     const double v = a.psm ? s3_candidate(a.psm, a.pmaxerr, c, a.L, a.ldc, a.e_bar) : a.pcand[c];
     const unsigned key = (unsigned(a.cs[c]) << 16) | unsigned(a.cr[c]);
     if (!(v < 0.0) && loop_better(v, c, bs, bi)) {
@@ -578,6 +582,7 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
       bk = ok;
     }
   }
+  __syncthreads();  // ss/si/sk may still be read from a previous call
   if (lane == 0) {
     ss[warp] = bs;
     si[warp] = bi;
@@ -608,13 +613,98 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   bi = si[0];
   bs = ss[0];
   bk = sk[0];
+}
+
+__global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
+  __shared__ double ss[32];
+  __shared__ int si[32];
+  __shared__ unsigned sk[32];
+  __shared__ int s_pos;
+  griddep_wait();
+  LoopState* st = a.st;
+  if (st->done) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int C = st->C, c0 = st->c0, c1 = st->c0 + st->Cl;
+  if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 0] = globaltimer();
+  // the commit's first reads (super-node map and active list, which only this
+  // kernel writes) are issued ahead of the argmin
+  const int sup0 = tid < a.n ? a.sup[tid] : -1;
+  const int sn0 = tid < st->ns ? a.sn[tid] : -1;
+  // argmin with the candidate's (s, r) carried along (no dependent load after it)
+  double bs;
+  int bi;
+  unsigned bk;
+  pick_block_argmin(a, c0, c1, ss, si, sk, bs, bi, bk);
+  const int L = a.L;
+  const double* wme = nullptr;  // the winner's max_err[L] (its rank's record), else pmaxerr
+  if (a.xch) {
+    // min-loc over ranks: every rank stores its record {smice, index, key,
+    // max_err[L]} into slot [parity][rank] of every rank's symmetric window
+    // (NVLink stores), the LSA barrier orders them, and every rank merges the
+    // same W records in rank order (lexicographic (smice, index); index < 0:
+    // no feasible candidate on that rank). Slots alternate with the iteration
+    // parity: a rank runs at most one barrier ahead of the slowest.
+    // xemul > 1 (one GPU, test aid): this rank plays xemul ranks, each
+    // reducing its own contiguous range into its own slot of the local window;
+    // the merge below is the multi-rank one.
+    const int par = st->iter & 1;
+    const int W = a.xemul > 1 ? a.xemul : a.world;
+    auto put = [&](char* dst, double vs, int vi, unsigned vk) {
+      *reinterpret_cast<double*>(dst) = vs;
+      *reinterpret_cast<long long*>(dst + 8) = vi;
+      *reinterpret_cast<unsigned*>(dst + 16) = vk;
+    };
+    auto me_of = [&](int l, int idx) {
+      return idx >= 0 ? (a.ldc > 0 ? a.pmaxerr[size_t(l) * a.ldc + idx] : a.pmaxerr[size_t(idx) * L + l]) : 0.0;
+    };
+    if (a.xemul > 1) {
+      for (int q = 0; q < W; ++q) {
+        const int xb = C / W, xe = C % W;
+        const int lo = q * xb + min(q, xe), hi = lo + xb + (q < xe ? 1 : 0);
+        double qs;
+        int qi;
+        unsigned qk;
+        pick_block_argmin(a, lo, hi, ss, si, sk, qs, qi, qk);
+        char* dst = static_cast<char*>(ncclGetLocalPointer(a.win, size_t(par * W + q) * a.rec_bytes));
+        if (tid == 0) put(dst, qs, qi, qk);
+        for (int l = tid; l < L; l += kLoopThreads) reinterpret_cast<double*>(dst + 24)[l] = me_of(l, qi);
+        __syncthreads();
+      }
+    } else {
+      const size_t my = size_t(par * W + a.rank) * size_t(a.rec_bytes);
+      for (int q = tid; q < W; q += kLoopThreads) put(static_cast<char*>(ncclGetLsaPointer(a.win, my, q)), bs, bi, bk);
+      for (int i = tid; i < W * L; i += kLoopThreads) {
+        const int q = i / L, l = i - q * L;
+        reinterpret_cast<double*>(static_cast<char*>(ncclGetLsaPointer(a.win, my, q)) + 24)[l] = me_of(l, bi);
+      }
+      ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), a.dcomm, ncclTeamLsa(a.dcomm), a.dcomm.lsaBarrier, 0);
+      bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    }
+    bs = __longlong_as_double(0x7ff0000000000000LL);
+    bi = -1;
+    bk = 0u;
+    int wq = -1;
+    for (int q = 0; q < W; ++q) {
+      const char* src = static_cast<const char*>(ncclGetLocalPointer(a.win, size_t(par * W + q) * a.rec_bytes));
+      const double qs = *reinterpret_cast<const volatile double*>(src);
+      const long long qi = *reinterpret_cast<const volatile long long*>(src + 8);
+      if (qi >= 0 && loop_better(qs, int(qi), bs, bi)) {
+        bs = qs;
+        bi = int(qi);
+        bk = *reinterpret_cast<const volatile unsigned*>(src + 16);
+        wq = q;
+      }
+    }
+    if (wq >= 0)
+      wme = reinterpret_cast<const double*>(
+          static_cast<const char*>(ncclGetLocalPointer(a.win, size_t(par * W + wq) * a.rec_bytes)) + 24);
+  }
   if (bi < 0) {  // no feasible assignment left (reduce.cpp:404)
     if (tid == 0) st->done = 1;
     return;
   }
   const int it = st->iter;
   const int s = int(bk >> 16), r = int(bk & 0xffffu);
-  const int L = a.L;
   if (it < a.cap) {
     if (tid == 0) {
       a.tr_sr[2 * it] = s;
@@ -624,7 +714,7 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
       a.tr_t[it] = globaltimer();
     }
     for (int l = tid; l < L; l += kLoopThreads) {
-      const double me = a.ldc > 0 ? a.pmaxerr[size_t(l) * a.ldc + bi] : a.pmaxerr[size_t(bi) * L + l];
+      const double me = wme ? wme[l] : (a.ldc > 0 ? a.pmaxerr[size_t(l) * a.ldc + bi] : a.pmaxerr[size_t(bi) * L + l]);
       a.tr_me[size_t(it) * L + l] = me;
       if (a.live_count) a.live_me[size_t(it) * L + l] = me;
     }

@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
       a.tdbg[size_t(a.st->iter) * kTdbg + 6] = t;
     }
-    C = a.st->C;
+    C = a.st->Cl;  // this rank's candidates (all of them on one GPU)
     R = a.st->R;
     gs = a.st->grp_start;
     gc = a.st->grp_cta;

@@ -131,6 +131,8 @@ class Engine {
   void set_profile(bool on);
   KernelStats stats(int which) const;  // 0 = scorer (score1 when it runs), 1 = base-refresh solve, 2 = score3 next to score1
   void set_exchange(int rank, int world, krg_exchange_fn fn, void* user);
+  // in-graph exchange over an NCCL communicator (unique_id: KRG_NCCL_ID_BYTES)
+  void set_comm(int rank, int world, const void* unique_id);
 
   // scenario voltages (V-hat) [L][3n][2]
   void scenario_voltages(double* out);

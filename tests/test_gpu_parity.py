@@ -406,3 +406,23 @@ def test_trace_csv_and_validate_report_bytes(case, tag, scen, flags, rad, tmp_pa
     res.write_trace_csv(str(out), zero_wall=True)
     assert out.read_text() == path(case, f"tracecsv_{tag}.csv").read_text()
     assert ctx.validate_report(res, 20) == path(case, f"validate_{tag}.csv").read_text()
+
+
+@pytest.mark.parametrize("case,tag,e_bar,emulate", [("c2", "mag_3e-3", 3e-3, 1), ("c2", "mag_3e-3", 3e-3, 2),
+                                                    ("c2", "mag_3e-3", 3e-3, 8), ("h2k", "mag_3e-3", 3e-3, 3),
+                                                    ("c1", "mag_1e-2", 1e-2, 5)])
+def test_in_graph_exchange(case, tag, e_bar, emulate, monkeypatch, tmp_path):
+    """Multi-GPU min-loc inside the loop graph (krg_set_comm): an NCCL
+    communicator, a symmetric window and an LSA barrier in the pick kernel.
+    One GPU: a one-rank communicator, playing `emulate` ranks (each reduces its
+    contiguous candidate range, parallel.cpp:21-29, into its own window slot;
+    the merge is the multi-rank one). Trajectory and reduced model bit-exact."""
+    monkeypatch.setenv("KRONRED_XCH_EMULATE", str(emulate))
+    ctx = kr.Context(host(case))
+    ctx.set_comm(0, 1, kr.nccl_unique_id())
+    for _ in range(2):  # graph instantiation, then the cached graph
+        res = ctx.run_reduction(kr.ReductionConfig(e_bar=e_bar))
+        assert_trace(res, case, tag)
+    out = tmp_path / "r.json"
+    res.write_reduced_json(str(out))
+    assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
