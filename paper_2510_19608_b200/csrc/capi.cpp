@@ -2,6 +2,7 @@
 // (include/kronred_b200.hpp): input parsing, problem construction and result
 // marshalling around the device Engine. Exceptions map to status codes the way
 // the reference CLI maps them to exit codes (main.cpp:234-246).
+#include <thread>
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -338,6 +339,53 @@ int device_from_env() {
   return -1;  // current device of the calling thread
 }
 
+// KRONRED_DEVICES="0,1,..." : run_reduction on several GPUs of this process
+// (the reference's worker split, parallel.cpp:11-34, across devices)
+std::vector<int> devices_from_env() {
+  std::vector<int> d;
+  if (const char* e = std::getenv("KRONRED_DEVICES")) {
+    std::string s(e);
+    size_t i = 0;
+    while (i < s.size()) {
+      const size_t j = s.find(',', i);
+      const std::string tok = s.substr(i, j == std::string::npos ? std::string::npos : j - i);
+      if (!tok.empty()) d.push_back(std::atoi(tok.c_str()));
+      if (j == std::string::npos) break;
+      i = j + 1;
+    }
+  }
+  return d;
+}
+
+// One engine and host thread per device, joined in one NCCL communicator;
+// every rank runs the device loop on its candidate range and the in-graph
+// exchange keeps them in lock step. Rank 0's result (identical on every
+// rank) is returned; the observer runs on rank 0's thread.
+void run_multi_device(const Problem& p, const std::vector<int>& devs, const ReductionConfig& cfg,
+                      const Engine::Observer& obs, ResultData& out) {
+  const int W = int(devs.size());
+  std::vector<std::unique_ptr<Engine>> engs(static_cast<size_t>(W));
+  std::vector<ResultData> res(static_cast<size_t>(W));
+  std::vector<std::string> err(static_cast<size_t>(W));
+  std::uint8_t id[KRG_NCCL_ID_BYTES];
+  if (krg_nccl_unique_id(id) != KRG_OK) throw Error("ncclGetUniqueId failed");
+  std::vector<std::thread> th;
+  for (int r = 0; r < W; ++r)
+    th.emplace_back([&, r] {
+      try {
+        engs[size_t(r)] = std::make_unique<Engine>(p, devs[size_t(r)]);
+        engs[size_t(r)]->set_comm(r, W, id);  // collective over the W threads
+        engs[size_t(r)]->run(cfg, r == 0 ? obs : Engine::Observer{}, res[size_t(r)]);
+      } catch (const std::exception& e) {
+        err[size_t(r)] = e.what();
+      }
+    });
+  for (std::thread& t : th) t.join();
+  for (int r = 0; r < W; ++r)
+    if (!err[size_t(r)].empty()) throw Error("rank " + std::to_string(r) + ": " + err[size_t(r)]);
+  out = std::move(res[0]);
+}
+
 // Engine cache of the C++ drop-in entry points (one per calling thread): the
 // reference signature builds its solver per call (reduce.cpp:359); here a call
 // on a network of the same STRUCTURE (node phases, slack, branch endpoints,
@@ -420,11 +468,16 @@ ReductionResult run_reduction(const Network& net, const ScenarioLibrary& lib, co
   if (!(cfg.e_bar >= 0)) throw ConfigError("e_bar must be non-negative");
   if (cfg.target_reduction && !(*cfg.target_reduction >= 0 && *cfg.target_reduction <= 1))
     throw ConfigError("target_reduction must lie in [0,1]");
-  Engine& eng = cached_engine(problem_from(net, &lib));
   ResultData rd;
   Engine::Observer obs;
   if (observer) obs = [&](const HostState& hs, const TraceRow& row) { observer(hs, row); };
-  eng.run(cfg, obs, rd);
+  const std::vector<int> devs = devices_from_env();
+  if (devs.size() > 1) {
+    run_multi_device(problem_from(net, &lib), devs, cfg, obs, rd);
+  } else {
+    Engine& eng = cached_engine(problem_from(net, &lib));
+    eng.run(cfg, obs, rd);
+  }
   ReductionResult res;
   res.model = std::move(rd.model);
   res.trace = std::move(rd.trace);
