@@ -163,6 +163,9 @@ int krg_nccl_unique_id(uint8_t* out /* KRG_NCCL_ID_BYTES */);
 int krg_set_comm(krg_ctx* ctx, int32_t rank, int32_t world, const uint8_t* unique_id);
 /* Number of kernels this context has launched so far. */
 int64_t krg_launch_count(const krg_ctx* ctx);
+/* 1 if the last krg_run_reduction ran as the device-resident loop graph (0:
+ * the host-driven loop: use_delta = false, KRONRED_LOOP=host, profiling). */
+int32_t krg_last_run_device_loop(const krg_ctx* ctx);
 /* Per-kernel CUDA-event timing on the launching stream (bench/roofline only):
  * which = 0 scorer (score1_kernel: |phi(r)| = 1 candidates, the dominant
  * kernel), 1 base-refresh solve, 2 score3_kernel (|phi(r)| >= 2 candidates

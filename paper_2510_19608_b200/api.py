@@ -98,6 +98,7 @@ _SIGS = [
     ("krg_selftest_cdiv", C.c_int, [C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double), C.c_int32]),
     ("krg_set_exchange", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, EXCHANGE_FN, C.c_void_p]),
     ("krg_nccl_unique_id", C.c_int, [C.c_char_p]),
+    ("krg_last_run_device_loop", C.c_int32, [C.c_void_p]),
     ("krg_set_comm", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p]),
     ("krg_launch_count", C.c_int64, [C.c_void_p]),
     ("krg_scenario_voltages", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
@@ -487,6 +488,11 @@ class Context:
     @property
     def L(self) -> int:
         return len(self.ids)
+
+    @property
+    def last_run_device_loop(self) -> bool:
+        """The last run_reduction ran as the device-resident loop graph."""
+        return bool(lib().krg_last_run_device_loop(self._h))
 
     def launch_count(self) -> int:
         return int(lib().krg_launch_count(self._h))

@@ -705,6 +705,7 @@ int krg_set_comm(krg_ctx* ctx, int32_t rank, int32_t world, const uint8_t* uniqu
 }
 
 int64_t krg_launch_count(const krg_ctx* ctx) { return ctx ? ctx->eng->launches() : 0; }
+int32_t krg_last_run_device_loop(const krg_ctx* ctx) { return ctx && ctx->eng->last_run_device_loop() ? 1 : 0; }
 
 int krg_set_profile(krg_ctx* ctx, int32_t on) {
   KRG_TRY

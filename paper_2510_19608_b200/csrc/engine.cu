@@ -176,7 +176,7 @@ struct Engine::Impl {
   // per-iteration inputs (pinned staging)
   DBuf<int4> d_cand;
   DBuf<unsigned> d_snt;
-  DBuf<int> d_snid, d_memoff, d_memlist;
+  DBuf<int> d_snid, d_memoff, d_memlist, d_snpos, d_memtmp;
   int4* h_cand = nullptr;
   unsigned* h_snt = nullptr;
   // magnitude path: active-row table + candidates grouped by |phi(r)|
@@ -432,7 +432,9 @@ struct Engine::Impl {
   const void* loop_key_bufs[kLoopKeyBufs] = {};
   int loop_key_L = -1;
   bool loop_key_live = false;
+  bool last_device_loop = false;  // the last run() took the device-resident loop graph
   ncclComm_t loop_key_comm = nullptr;
+  int loop_key_cplx = -1;
   DBuf<unsigned long long> d_tdbg;
   bool loop_trace = std::getenv("KRONRED_LOOP_TRACE") != nullptr;
   bool force_host_loop = std::getenv("KRONRED_LOOP") != nullptr && std::string(std::getenv("KRONRED_LOOP")) == "host";
@@ -1455,6 +1457,37 @@ struct Engine::Impl {
     }
   }
 
+  // complex-objective scorer geometry and buffers for C candidates
+  ScoreArgs members_args(long long C) {
+    ScoreArgs a{};
+    a.C = int(C);
+    a.L = L;
+    a.nphi = nphi;
+    a.ns = int(hs.supernodes.size());
+    int P = L * (32 / gcd_int(L, 32));
+    if (P > 512) P = L;
+    a.G = P / L;
+    const long long ctas = (C + a.G - 1) / a.G;
+    const int smax = std::max(1, 512 / P);
+    const long long want = (148LL * 1536 + ctas * P - 1) / (ctas * P);
+    a.S = int(std::min<long long>(smax, std::max<long long>(1, want)));
+    a.K = 64;
+    a.cand = d_cand.p;
+    a.snt = d_snt.p;
+    a.mask = d_mask.p;
+    a.prow_off = d_prow_off.p;
+    a.Z = d_Z.p;
+    a.bv = d_bv.p;
+    a.iagg = d_iagg.p;
+    a.mem_off = d_memoff.p;
+    a.mem_list = d_memlist.p;
+    a.sn_id = d_sn.p;
+    a.vhatp = d_vhatp.p;
+    a.out_smice = d_psmice.p;
+    a.out_maxerr = d_pmaxerr.p;
+    return a;
+  }
+
   void launch_score_members(long long C) {
     ScoreArgs a{};
     a.C = int(C);
@@ -1555,7 +1588,7 @@ struct Engine::Impl {
   size_t enum_smem() const { return (enum_kcap() + 2 * prob.net.branches.size() + 1) * sizeof(unsigned); }
 
   bool device_loop_ok(const ReductionConfig& c) const {
-    return !force_host_loop && c.use_delta && c.objective == Objective::magnitude && (world == 1 || comm) && !profile &&
+    return !force_host_loop && c.use_delta && (world == 1 || comm) && !profile &&
            full.bW > 0 && n <= 65535 && enum_smem() + 24 * 1024 <= size_t(optin_smem);
   }
 
@@ -1578,6 +1611,13 @@ struct Engine::Impl {
     a.fill = s3_fill();
     a.force_s = s3_force;
     a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
+    a.complex_obj = cfg.objective == Objective::complex_error ? 1 : 0;
+    a.psm = a.complex_obj ? d_psmice.p : nullptr;  // complex: per-pair sums in the pick
+    a.snt = d_snt.p;
+    a.sn_pos = d_snpos.p;
+    a.mem_off = d_memoff.p;
+    a.mem_list = d_memlist.p;
+    a.mem_tmp = d_memtmp.p;
     a.rank = comm ? rank : 0;
     a.world = comm ? world : 1;
     a.xch = comm ? 1 : 0;
@@ -1649,6 +1689,8 @@ struct Engine::Impl {
       CK(cudaFuncSetAttribute(enum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(enum_smem())));
     }
     d_loopst.alloc(1);
+    d_snpos.alloc(size_t(n));
+    d_memtmp.alloc(size_t(n));
     d_sup.alloc(size_t(n));
     d_sn.alloc(size_t(n));
     d_tabnode.alloc(size_t(n));
@@ -1671,6 +1713,13 @@ struct Engine::Impl {
         bt[size_t(b)] = prob.net.branches[size_t(b)].to;
       }
       CK(cudaMemcpyAsync(d_sup.p, ident.data(), sizeof(int) * size_t(n), cudaMemcpyHostToDevice, stream));
+      if (cfg.objective == Objective::complex_error) {  // every node its own cluster
+        std::vector<int> off(static_cast<size_t>(n) + 1);
+        std::iota(off.begin(), off.end(), 0);
+        CK(cudaMemcpyAsync(d_memlist.p, ident.data(), sizeof(int) * size_t(n), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemcpyAsync(d_memoff.p, off.data(), sizeof(int) * (size_t(n) + 1), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));  // pageable sources
+      }
       CK(cudaMemcpyAsync(d_sn.p, ident.data(), sizeof(int) * size_t(n), cudaMemcpyHostToDevice, stream));
       if (nb) {
         CK(cudaMemcpyAsync(d_brf.p, bf.data(), sizeof(int) * size_t(nb), cudaMemcpyHostToDevice, stream));
@@ -1734,6 +1783,7 @@ struct Engine::Impl {
     const bool key_ok = loop_exec && loop_key_ebar == cfg.e_bar && loop_key_has == la.has_target &&
                         loop_key_target == la.target && loop_key_trace == loop_trace && loop_key_L == L &&
                         loop_key_live == (la.live_count != nullptr) && loop_key_comm == comm &&
+                        loop_key_cplx == la.complex_obj &&
                         std::equal(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     if (!key_ok) {
       if (loop_exec) CK(cudaGraphExecDestroy(loop_exec));
@@ -1770,7 +1820,8 @@ struct Engine::Impl {
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       const int items_max = 4 * ((2 * nb + 4) / 5 + 3) * s3_nsl();  // up to 4 lanes per pair
       const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
-      const bool s1 = s1_ok();
+      const bool cplx = cfg.objective == Objective::complex_error;
+      const bool s1 = s1_ok() && !cplx;  // (every created handle must drive a node)
       // one switch handle per unrolled copy (a handle drives one conditional
       // node); the enumeration of copy u sets copy u + 1's
       cudaGraphConditionalHandle hsw[kLoopUnroll] = {};
@@ -1791,8 +1842,26 @@ struct Engine::Impl {
           CK(cudaEventCreateWithFlags(&ev_join3, cudaEventDisableTiming));
         }
       }
+      ScoreArgs qc{};
+      int gridc = 0, threadsc = 0;
+      size_t smemc = 0;
+      if (cplx) {
+        qc = members_args(int(2 * nb + 1));
+        if (const char* e = std::getenv("KRONRED_CPLX_K")) qc.K = std::max(1, std::atoi(e));  // tuning aid
+        qc.st = d_loopst.p;
+        qc.ldc = s3_ldc();
+        qc.cidx = d_cidx.p;
+        const int P = qc.G * L;
+        threadsc = P * qc.S;
+        smemc = size_t(std::max(qc.K, qc.S)) * size_t(P) * sizeof(double);
+        int occc = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occc, score_kernel<true>, threadsc, smemc));
+        gridc = std::max(1, std::min((2 * nb + qc.G) / qc.G, std::max(1, occc) * sms));
+      }
       for (int u = 0; u < kLoopUnroll; ++u) {
-      if (s1) {
+      if (cplx) {
+        score_kernel<true><<<gridc, threadsc, smemc, stream>>>(qc);
+      } else if (s1) {
         // |phi(r)| >= 2 candidates (score3) next to the |phi(r)| = 1 ones
         // (score1<S>, S picked by the enumeration through a switch node)
         CK(cudaEventRecord(ev_fork3, stream));
@@ -1811,7 +1880,7 @@ struct Engine::Impl {
       // pick and refresh follow their stream predecessor by programmatic
       // dependent launch (launch overlapped with the predecessor's tail; each
       // waits on griddepcontrol before reading its results)
-      launch_dep(pdl && !s1, pick_commit_kernel, dim3(1), dim3(kLoopThreads), 0, stream, lb);
+      launch_dep(pdl && !s1 && !cplx, pick_commit_kernel, dim3(1), dim3(kLoopThreads), 0, stream, lb);
       CK(cudaEventRecord(ev_fork, stream));
       CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
       enum_kernel<<<1, kLoopThreads, enum_smem(), stream2>>>(lb);
@@ -1833,6 +1902,7 @@ struct Engine::Impl {
       loop_key_L = L;
       loop_key_live = la.live_count != nullptr;
       loop_key_comm = comm;
+      loop_key_cplx = la.complex_obj;
       std::copy(bufs, bufs + kLoopKeyBufs, loop_key_bufs);
     }
     // the whole loop: one graph launch (a loop that is already done runs one
@@ -1892,7 +1962,7 @@ struct Engine::Impl {
     check_deferred_fail();
     const LoopState st = *h_loopst;
     // kernels per loop-body iteration: scorer(s), pick, enumeration, refresh
-    launches += (s1_ok() ? 5LL : 4LL) * ((st.iter + kLoopUnroll) / kLoopUnroll * kLoopUnroll);
+    launches += (s1_ok() && cfg.objective == Objective::magnitude ? 5LL : 4LL) * ((st.iter + kLoopUnroll) / kLoopUnroll * kLoopUnroll);
     const int it = st.iter;
     if (loop_trace && it > 2) {
       std::vector<unsigned long long> T(size_t(n + 1) * kTdbg);
@@ -1987,6 +2057,7 @@ KernelStats Engine::stats(int which) const {
 }
 const Problem& Engine::problem() const { return impl_->prob; }
 std::int64_t Engine::launches() const { return impl_->launches; }
+bool Engine::last_run_device_loop() const { return impl_->last_device_loop; }
 
 void Engine::set_comm(int rank, int world, const void* unique_id) {
   ncclUniqueId id;
@@ -2238,6 +2309,7 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
   CK(cudaEventRecord(I.ev_run0, I.stream));
   I.begin(cfg);
   int iteration = 0;
+  I.last_device_loop = I.device_loop_ok(cfg);
   if (!I.device_loop_ok(cfg)) {  // host-driven loop: surface a singular factorization first
     CK(cudaStreamSynchronize(I.stream));
     I.check_deferred_fail();

@@ -82,6 +82,15 @@ struct LoopArgs {
   ncclWindow_t win;
   int rec_bytes;              // per-rank record: {smice, index, key, pad, max_err[L]}
   int xemul;                  // > 1: one GPU plays xemul ranks (test aid, KRONRED_XCH_EMULATE)
+  // complex objective (score_kernel<true>): super-node table of the active
+  // list, each node's position in it, members of every super-node (CSR by
+  // node id, kept in step with commit)
+  int complex_obj;
+  unsigned* snt;              // [n] (rho0 << 3) | mask per active super-node
+  int* sn_pos;                // [n] position of an active super-node in sn
+  int* mem_off;               // [n + 1]
+  int* mem_list;              // [n]
+  int* mem_tmp;               // [n] scratch of the member move
   volatile int* live_count;
   int* live_src;              // [cap][3]: s, r, candidate count
   double* live_smice;         // [cap]
@@ -201,6 +210,12 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
 #ifdef ENUM_TIMING
   if (tid == 0) et[0] = clock64();
 #endif
+  if (a.complex_obj)  // complex scorer: active super-node table and positions
+    for (int k = tid; k < ns; k += kLoopThreads) {
+      const int i = a.sn[k];
+      a.sn_pos[i] = k;
+      a.snt[k] = (unsigned(a.prow_off[i]) << 3) | unsigned(a.mask[i]);
+    }
   // ---- row table over the active super-nodes ------------------------------
   const int ch = (ns + kLoopThreads - 1) / kLoopThreads;
   const int b0 = min(ns, tid * ch), b1 = min(ns, b0 + ch);
@@ -495,7 +510,8 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
     if (r0 + tid < Cl) {
       const unsigned bg = g == 1 ? b1 : (g == 2 ? b2 : b3);
       const int p = s_wcnt[warp][g] + __popc(bg & lane_lt);
-      a.cand[p] = make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
+      a.cand[p] = a.complex_obj ? make_int4(s, r, a.sn_pos[s], a.sn_pos[r])
+                                : make_int4(s, r, a.tab_of_node[s], a.tab_of_node[r]);
       a.cidx[p] = i;
     }
     __syncthreads();  // s_wcnt is rewritten next round
@@ -748,6 +764,28 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   }
   for (int j = tid; j < a.n; j += kLoopThreads)
     if ((j == tid ? sup0 : a.sup[j]) == r) a.sup[j] = s;
+  if (a.complex_obj) {
+    // members: r's list joins the end of s's (reduce.cpp:326-329 append
+    // order), the lists between the two move by |members(r)|
+    const int os0 = a.mem_off[s], os1 = a.mem_off[s + 1], or0 = a.mem_off[r], or1 = a.mem_off[r + 1];
+    const int kr = or1 - or0;
+    const int A = s < r ? os1 : or0, B = s < r ? or1 : os1;
+    for (int x = A + tid; x < B; x += kLoopThreads) {
+      int src;
+      if (s < r)  // [r's members][lists s+1 .. r-1]
+        src = x - A < kr ? or0 + (x - A) : x - kr;
+      else  // [lists r+1 .. s][r's members]
+        src = x < B - kr ? x + kr : or0 + (x - (B - kr));
+      a.mem_tmp[x] = a.mem_list[src];
+    }
+    __syncthreads();
+    for (int x = A + tid; x < B; x += kLoopThreads) a.mem_list[x] = a.mem_tmp[x];
+    if (s < r)
+      for (int i = s + 1 + tid; i <= r; i += kLoopThreads) a.mem_off[i] += kr;
+    else
+      for (int i = r + 1 + tid; i <= s; i += kLoopThreads) a.mem_off[i] -= kr;
+    (void)os0;
+  }
   // remove r from the ascending active list
   const int ns = st->ns;
   for (int k = tid; k < ns; k += kLoopThreads)

@@ -128,6 +128,7 @@ class Engine {
 
   const Problem& problem() const;
   std::int64_t launches() const;
+  bool last_run_device_loop() const;
   void set_profile(bool on);
   KernelStats stats(int which) const;  // 0 = scorer (score1 when it runs), 1 = base-refresh solve, 2 = score3 next to score1
   void set_exchange(int rank, int world, krg_exchange_fn fn, void* user);

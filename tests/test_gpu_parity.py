@@ -426,3 +426,18 @@ def test_in_graph_exchange(case, tag, e_bar, emulate, monkeypatch, tmp_path):
     out = tmp_path / "r.json"
     res.write_reduced_json(str(out))
     assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
+
+
+@pytest.mark.parametrize("case,tag", [("c1", "complex_1e-3"), ("m40", "complex_1e-3"), ("c2", "complex_3e-3")])
+def test_complex_objective_device_loop(case, tag, tmp_path):
+    """The complex objective (reduce.cpp:99-107) inside the device loop: the
+    persistent member-walking scorer, device-side member lists moved on
+    commit; trajectory, scores and reduced model bit for bit, and the same
+    trace as the host-driven loop."""
+    ctx = kr.Context(host(case))
+    res = ctx.run_reduction(kr.ReductionConfig(e_bar=float(tag.split("_")[1]), objective="complex"))
+    assert ctx.last_run_device_loop
+    assert_trace(res, case, tag)
+    out = tmp_path / "r.json"
+    res.write_reduced_json(str(out))
+    assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
