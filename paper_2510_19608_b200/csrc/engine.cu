@@ -1085,6 +1085,7 @@ struct Engine::Impl {
     CK(cudaFuncSetAttribute(base_refresh_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(base_refresh_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(naive_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
+    CK(cudaFuncSetAttribute(naive_score_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     n = prob.y.n;
     prow_off.assign(size_t(n) + 1, 0);
     for (int i = 0; i < n; ++i) {
@@ -1226,8 +1227,8 @@ struct Engine::Impl {
     if (c.target_reduction && !(*c.target_reduction >= 0 && *c.target_reduction <= 1))
       throw ConfigError("target_reduction must lie in [0,1]");
     if (L == 0) throw ValidationError("scenario library is empty");
-    if (!c.use_delta && (full.bW <= 0 || !full.bsm))
-      throw ConfigError("use_delta=false needs the factor program in shared memory (network too large)");
+    if (!c.use_delta && full.bW <= 0)
+      throw ConfigError("use_delta=false: the solution vector does not fit in shared memory");
     cfg = c;
     // AnchoredSolver (re-factorized per run, as run_reduction does, reduce.cpp:359)
     factorize(full, d_yin.p, pivot_floor, /*check_now=*/false);
@@ -1361,7 +1362,39 @@ struct Engine::Impl {
         W = w;
         break;
       }
-    if (W == 0) throw ConfigError("use_delta=false: the factor program does not fit in shared memory");
+    if (W == 0 || !full.bsm || std::getenv("KRONRED_NAIVE_GLOBAL")) {
+      // program too large for shared memory: read it from global memory, one
+      // pair per CTA of WB warps (the layout of the global refresh program)
+      NaiveArgs q{};
+      b.W = 1;
+      q.b = b;
+      q.C = int(C);
+      q.cs = d_cs.p;
+      q.cr = d_cr.p;
+      q.ns = int(hs.supernodes.size());
+      q.sn_id = d_snid.p;
+      q.mem_off = d_memoff.p;
+      q.mem_list = d_memlist.p;
+      q.mask = d_mask.p;
+      q.prow_off = d_prow_off.p;
+      q.vhat_full = d_vhat.p;
+      q.n = n;
+      q.e_bar = cfg.e_bar;
+      q.complex_obj = cfg.objective == Objective::complex_error ? 1 : 0;
+      q.out_sm = d_psmice.p;
+      q.out_mx = d_pmaxerr.p;
+      q.ldc = s3_ldc();
+      const size_t sm = size_t(nphi) * 16 + size_t(n) * 8;
+      if (sm > size_t(optin_smem) - 64) throw ConfigError("use_delta=false: the solution vector does not fit in shared memory");
+      int sms = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+      const long long pairs = C * L;
+      const int grid = int(std::max<long long>(1, std::min<long long>(pairs, 2LL * sms)));
+      naive_score_global_kernel<<<grid, 32 * std::max(1, b.WB), sm, stream>>>(q);
+      launched();
+      CK(cudaGetLastError());
+      return;
+    }
     b.W = W;
     NaiveArgs q{};
     q.b = b;

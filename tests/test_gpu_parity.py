@@ -37,6 +37,17 @@ def cfg_from_flags(flags: list[str]) -> kr.ReductionConfig:
     return c
 
 
+def strip_workers(flags: list[str]) -> list[str]:
+    """Drop the reference's `--workers N` (thread count; no GPU meaning)."""
+    out, it = [], iter(flags)
+    for f in it:
+        if f == "--workers":
+            next(it)
+        else:
+            out.append(f)
+    return out
+
+
 def bits(x: float) -> str:
     return d2h(float(x))
 
@@ -242,7 +253,7 @@ def test_large_feeders_bitwise(case, tag, meta, tmp_path):
     runs to the 90 % / 80 % targets where committed, else the first
     iterations), its final errors, and its reduced-model JSON byte for byte."""
     ctx = kr.Context(host(case))
-    res = ctx.run_reduction(cfg_from_flags([f for f in meta["flags"] if f not in ("--workers", "0")]))
+    res = ctx.run_reduction(cfg_from_flags(strip_workers(meta["flags"])))
     assert_trace(res, case, tag)
     try:
         want = path(case, f"reduced_{tag}.json")
@@ -292,7 +303,7 @@ def test_regenerated_libraries_bitwise(case, tmp_path):
     assert (tmp_path / "net.json").read_bytes() == path("c4", "net.json").read_bytes()
     ctx = kr.Context(kr.HostProblem(str(path("c4", "net.json")), str(scen)))
     for tag, meta in runs(case).items():
-        res = ctx.run_reduction(cfg_from_flags([f for f in meta["flags"] if f not in ("--workers", "0")]))
+        res = ctx.run_reduction(cfg_from_flags(strip_workers(meta["flags"])))
         assert_trace(res, case, tag)
 
 
@@ -441,3 +452,17 @@ def test_complex_objective_device_loop(case, tag, tmp_path):
     out = tmp_path / "r.json"
     res.write_reduced_json(str(out))
     assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
+
+
+@pytest.mark.parametrize("case,tag,global_prog", [("c1", "naive_mag_1e-3", True), ("c1", "naive_complex_1e-3", True),
+                                                  ("m40", "naive_mag_1e-3", True)])
+def test_naive_program_from_global_memory(case, tag, global_prog, monkeypatch):
+    """use_delta = false with the factor program read from global memory (the
+    path of networks whose program does not fit in shared memory; forced here
+    with KRONRED_NAIVE_GLOBAL): the reference's full-solve traces bit for bit.
+    The 5,991-node case runs it without forcing (test_large_feeders_bitwise)."""
+    if global_prog:
+        monkeypatch.setenv("KRONRED_NAIVE_GLOBAL", "1")
+    (meta,) = [m for t, m in runs(case).items() if t == tag]
+    res = kr.Context(host(case)).run_reduction(cfg_from_flags(meta["flags"]))
+    assert_trace(res, case, tag)
