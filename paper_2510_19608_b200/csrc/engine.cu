@@ -1899,7 +1899,24 @@ struct Engine::Impl {
         // (score1<S>, S picked by the enumeration through a switch node)
         CK(cudaEventRecord(ev_fork3, stream));
         CK(cudaStreamWaitEvent(stream3, ev_fork3, 0));
-        score3_kernel<<<grid3, s3_threads(), sm3, stream3>>>(q);
+        {
+          // the multi-phase items are few and latency-bound (each walks every
+          // row): highest priority, so their CTAs are resident before the
+          // wide score1 grid fills the SMs
+          cudaLaunchConfig_t lc{};
+          lc.gridDim = dim3(grid3);
+          lc.blockDim = dim3(s3_threads());
+          lc.dynamicSmemBytes = sm3;
+          lc.stream = stream3;
+          cudaLaunchAttribute at[1];
+          int lo = 0, hi = 0;
+          CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+          at[0].id = cudaLaunchAttributePriority;
+          at[0].val.priority = std::getenv("KRONRED_NO_PRIO") ? lo : hi;
+          lc.attrs = at;
+          lc.numAttrs = 1;
+          CK(cudaLaunchKernelEx(&lc, score3_kernel, q));
+        }
         lb.scond = hsw[(u + 1) % kLoopUnroll];  // set by this copy's enumeration
         add_switch(stream, hsw[u], [&](int i, cudaStream_t cs) {
           const int Si = i == 0 ? 1 : (i == 1 ? 2 : 4);
