@@ -466,3 +466,24 @@ def test_naive_program_from_global_memory(case, tag, global_prog, monkeypatch):
     (meta,) = [m for t, m in runs(case).items() if t == tag]
     res = kr.Context(host(case)).run_reduction(cfg_from_flags(meta["flags"]))
     assert_trace(res, case, tag)
+
+
+@pytest.mark.parametrize("case,tag,flags", [("c1", "mag_1e-3", ["--e-bar", "1e-3"]),
+                                            ("c1", "rad_1e-2_t06", ["--e-bar", "1e-2", "--target", "0.6", "--radialize"]),
+                                            ("c2", "mag_3e-3", ["--e-bar", "3e-3"])])
+def test_reference_shim_relinks_reference_binary(case, tag, flags, tmp_path):
+    """integration/reference_shim.cpp: the reference's own driver (oracle/
+    ref_driver.cpp over the unmodified reference library) relinked so that
+    kronred::run_reduction forwards to this library's C ABI (oracle/Makefile
+    target `shim`). Its observer-streamed trace and reduced model are the
+    reference's, bit for bit."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "shim_ref"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/shim_ref not built (make -C oracle shim)")
+    out, tr = tmp_path / "r.json", tmp_path / "t.txt"
+    subprocess.run([str(exe), "reduce", "--net", str(path(case, "net.json")), "--scen", str(path(case, "scen.csv")),
+                    *flags, "--reduced", str(out), "--trace-hex", str(tr)], check=True, capture_output=True)
+    assert out.read_text() == path(case, f"reduced_{tag}.json").read_text()
+    assert tr.read_text() == path(case, f"trace_{tag}.txt").read_text()
