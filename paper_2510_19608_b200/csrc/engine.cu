@@ -216,7 +216,9 @@ struct Engine::Impl {
     if (const char* e = std::getenv("KRONRED_S3_FILL")) return std::atoll(e);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return (long long)sms * 3 * 128;
+    // score1 (small networks): split once pairs x lanes fit one wave of 3
+    // resident CTAs per SM; score3 on large networks: about one CTA per SM
+    return s1_ok() ? (long long)sms * 3 * 128 : (long long)sms * 128;
   }
   // slice-completion counters: one per candidate group at the widest split
   size_t s3_groups_max() const {
@@ -239,7 +241,6 @@ struct Engine::Impl {
     q.nphi = nphi;
     q.G = s3_slots();
     q.S = 1;
-    q.ns_max = std::getenv("KRONRED_S3_NS") ? std::max(3, std::atoi(std::getenv("KRONRED_S3_NS"))) : 8;
     q.s_multi = s3_multi_lanes();
     q.Ls = s3_ls();
     q.nsl = s3_nsl();
@@ -263,8 +264,12 @@ struct Engine::Impl {
 
   // score1 (kernels_score1.cuh) takes the |phi(r)| = 1 candidates when the
   // scorer runs its default geometry (16 slots, slices of 8 scenarios)
+  // (small networks: Z L2-resident; on large ones the wider score3 items
+  // share more staging and measure faster: tools/large_ab.py)
   bool s1_ok() const {
-    return s3_ls() == kS1Ls && s3_slots() == kS1G && L <= 128 && std::getenv("KRONRED_NO_S1") == nullptr;
+    if (std::getenv("KRONRED_NO_S1")) return false;
+    const bool fits = size_t(nphi) * size_t(nphi) * 16 <= (size_t(64) << 20) || std::getenv("KRONRED_FORCE_S1");
+    return s3_ls() == kS1Ls && s3_slots() == kS1G && L <= 128 && fits;
   }
   // candidates per score1 item at S = 1, 2, 4 (KRONRED_S1_GK="8,8,4" tuning;
   // supported: 16/8 at S = 1 and 2, 8/4 at S = 4)
@@ -1081,7 +1086,8 @@ struct Engine::Impl {
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
     for (auto fn : {score_kernel<false>, score_kernel<true>})
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem));
-    CK(cudaFuncSetAttribute(score3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 256));
+    CK(cudaFuncSetAttribute(score3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 256));
+    CK(cudaFuncSetAttribute(score3_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 256));
     CK(cudaFuncSetAttribute(base_refresh_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(base_refresh_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
     CK(cudaFuncSetAttribute(naive_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem - 64));
@@ -1457,7 +1463,7 @@ struct Engine::Impl {
         }
         q.skip_nl1 = 1;
         if (c3 > q.grp_cta[1]) {
-          score3_kernel<<<c3 - q.grp_cta[1], s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
+          score3_kernel<0><<<c3 - q.grp_cta[1], s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
           launched();
           CK(cudaGetLastError());
         }
@@ -1472,7 +1478,10 @@ struct Engine::Impl {
         }
         return;
       } else if (c3 > 0) {
-        score3_kernel<<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
+        if (q.S == 1)
+          score3_kernel<1><<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
+        else
+          score3_kernel<0><<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
         launched();
         CK(cudaGetLastError());
       }
@@ -1848,7 +1857,7 @@ struct Engine::Impl {
       q.tdbg = la.tdbg;
       int occ = 0;
       const size_t sm3 = S3Layout{s3_ls(), s3_slots()}.smem_bytes();
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score3_kernel, s3_threads(), sm3));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score3_kernel<0>, s3_threads(), sm3));
       int sms = 0;
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       const int items_max = 4 * ((2 * nb + 4) / 5 + 3) * s3_nsl();  // up to 4 lanes per pair
@@ -1858,7 +1867,7 @@ struct Engine::Impl {
       // one switch handle per unrolled copy (a handle drives one conditional
       // node); the enumeration of copy u sets copy u + 1's
       cudaGraphConditionalHandle hsw[kLoopUnroll] = {};
-      if (s1) {
+      if (!cplx) {
         // first iteration's split: the candidate count of iteration 1 is a
         // property of the network (the graph is keyed on it)
         std::vector<int> c0s, c0r;
@@ -1868,7 +1877,7 @@ struct Engine::Impl {
           CK(cudaGraphConditionalHandleCreate(&hsw[u], body, unsigned(u == 0 ? s1_switch_index(S0) : 0),
                                               cudaGraphCondAssignDefault));
         lb.use_scond = 1;
-        q.skip_nl1 = 1;
+        q.skip_nl1 = s1 ? 1 : 0;
         if (!stream3) {
           CK(cudaStreamCreateWithFlags(&stream3, cudaStreamNonBlocking));
           CK(cudaEventCreateWithFlags(&ev_fork3, cudaEventDisableTiming));
@@ -1915,7 +1924,7 @@ struct Engine::Impl {
           at[0].val.priority = std::getenv("KRONRED_NO_PRIO") ? lo : hi;
           lc.attrs = at;
           lc.numAttrs = 1;
-          CK(cudaLaunchKernelEx(&lc, score3_kernel, q));
+          CK(cudaLaunchKernelEx(&lc, score3_kernel<0>, q));
         }
         lb.scond = hsw[(u + 1) % kLoopUnroll];  // set by this copy's enumeration
         add_switch(stream, hsw[u], [&](int i, cudaStream_t cs) {
@@ -1925,7 +1934,17 @@ struct Engine::Impl {
         CK(cudaEventRecord(ev_join3, stream3));
         CK(cudaStreamWaitEvent(stream, ev_join3, 0));
       } else {
-        launch_dep(pdl && pdl_score, score3_kernel, dim3(grid3), dim3(s3_threads()), sm3, stream, q);
+        // every candidate in score3: the split picks the compiled S = 1 kernel
+        // or the run-time split one
+        lb.scond = hsw[(u + 1) % kLoopUnroll];
+        add_switch(stream, hsw[u], [&](int i, cudaStream_t cs) {
+          if (i == 0)
+            score3_kernel<1><<<grid3, s3_threads(), sm3, cs>>>(q);
+          else
+            score3_kernel<0><<<grid3, s3_threads(), sm3, cs>>>(q);
+          launched();
+          CK(cudaGetLastError());
+        });
       }
       // pick and refresh follow their stream predecessor by programmatic
       // dependent launch (launch overlapped with the predecessor's tail; each

@@ -766,9 +766,22 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
 template <bool SM>
 __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   extern __shared__ __align__(16) double2 smem[];
-  __shared__ unsigned long long bar;
+  __shared__ unsigned long long bar, bar_prog;
+  // The factor and the program never change during a run: with programmatic
+  // dependent launch their TMA staging starts before the wait on the pick
+  // kernel (which triggers its dependents early), overlapping its commit.
+  if (SM && threadIdx.x == 0) {
+    mbar_init(&bar_prog, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar_prog, unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u);
+    if (a.ncf) bulk_g2s(smem, a.cfac, unsigned(a.ncf) * 16u, &bar_prog);
+    bulk_g2s(reinterpret_cast<int*>(smem + a.ncf), a.meta, unsigned(a.nmeta) * 4u, &bar_prog);
+  }
   griddep_wait();
-  if (a.st && a.st->done) return;
+  if (a.st && a.st->done) {
+    if (SM) mbar_wait(&bar_prog, 0);  // no copy may outlive the CTA
+    return;
+  }
   if (a.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -790,13 +803,8 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     // incremental: x <- last forward values, and the right-hand sides of the
     // re-eliminated path nodes from a second buffer (both TMA-staged)
     const unsigned per = unsigned(a.nphi) * 16u;
-    const unsigned bytes = (SM ? unsigned(a.ncf) * 16u + unsigned(a.nmeta) * 4u : 0u) +
-                           unsigned(nw) * per * (stage_rhs ? 2u : 1u);
+    const unsigned bytes = unsigned(nw) * per * (stage_rhs ? 2u : 1u);
     mbar_expect_tx(&bar, bytes);
-    if (SM) {
-      if (a.ncf) bulk_g2s(smem, a.cfac, unsigned(a.ncf) * 16u, &bar);
-      bulk_g2s(reinterpret_cast<int*>(smem + a.ncf), a.meta, unsigned(a.nmeta) * 4u, &bar);
-    }
     const double2* src = a.inc ? a.tfwd : a.iaggp;
     for (int w = 0; w < nw; ++w)
       bulk_g2s(xall + size_t(w) * a.nphi, src + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
@@ -805,6 +813,7 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
         bulk_g2s(xall + size_t(a.W + w) * a.nphi, a.iaggp + size_t(blockIdx.x * a.W + w) * a.nphi, per, &bar);
   }
   __syncthreads();
+  if (SM) mbar_wait(&bar_prog, 0);
   mbar_wait(&bar, 0);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[0] = clock64();
   if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 8] = globaltimer_ns();

@@ -637,6 +637,10 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   __shared__ unsigned sk[32];
   __shared__ int s_pos;
   griddep_wait();
+  // let the base refresh (the next kernel, launched programmatically) start
+  // staging its constant program now; it waits for this grid before reading
+  // anything the commit writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   LoopState* st = a.st;
   if (st->done) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -45,7 +45,6 @@ struct S3Args {
   int C, L, nphi, R;
   int G;                     // Z column slots per CTA (candidates per CTA = G / |phi(r)| / S)
   int S;                     // lanes per pair (host-driven loop; the device loop reads st->S)
-  int ns_max;                // staging ring: most slots an item may carve (>= 3)
   int skip_nl1;              // 1: leave the |phi(r)| = 1 items to score1_kernel
   int s_multi;               // lanes per pair of the |phi(r)| >= 2 items when skip_nl1
   int Ls, nsl;               // scenario slice width and slice count
@@ -304,11 +303,10 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
   const int c = g_begin + min(cg, g_count - 1);
   const S3Layout lay{Ls, a.G};
   double2* base2 = reinterpret_cast<double2*>(smd);
-  // staging ring: the allocation holds 3 slots of the widest item (G Z-column
-  // slots); an item with fewer candidates (row split) carves it into more,
-  // smaller slots, so more tiles are in flight while a slot computes
+  // staging ring: 3 slots sized for this item's candidates (a deeper ring
+  // measured no faster: the copy latency is covered by one tile's compute)
   const size_t buf_e = lay.tab_e() + lay.bv_e() + size_t(Gk) * (NL * 2 * K3 + 1);
-  const int NS = max(3, min(a.ns_max, int(3 * lay.buf_e() / buf_e)));
+  constexpr int NS = 3;
   auto tab_s = [&](int b) { return reinterpret_cast<unsigned*>(base2 + b * buf_e); };
   auto bv_s = [&](int b) { return base2 + b * buf_e + lay.tab_e(); };
   auto z_s = [&](int b) { return base2 + b * buf_e + lay.tab_e() + lay.bv_e(); };
@@ -459,21 +457,23 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
 #ifdef S3_TIMING  // tuning aid: per-phase cycle counts of CTA 0's warps
   long long tm_pro = clock64(), tm_wait = 0, tm_stage = 0, tm_rho = 0, tm_fd = 0, tm_comp = 0, tm_x;
 #endif
-  // prologue: tiles 0 .. NS-2 in flight (one commit group each, empty past
-  // the end), then wait for tile 0
-  for (int t = 0; t < NS - 1; ++t) {
-    if (t < ntiles) {
-      if (fst) {
-        load_rho(t, rn);
-        stage_fast(t, t, rn);
-      } else {
-        stage(t, t);
-      }
-    }
+  // prologue: tiles 0 and 1 in flight, then wait for tile 0
+  if (fst) {
+    unsigned r0[3], r1[3];
+    load_rho(0, r0);
+    load_rho(1, r1);
+    stage_fast(0, 0, r0);
+    cp_async_commit();
+    if (ntiles > 1) stage_fast(1, 1, r1);
+    cp_async_commit();
+    load_rho(2, rn);
+  } else {
+    stage(0, 0);
+    cp_async_commit();
+    if (ntiles > 1) stage(1, 1);
     cp_async_commit();
   }
-  if (fst) load_rho(NS - 1, rn);
-  cp_async_wait_pending(NS - 2);
+  cp_async_wait1();
   __syncthreads();
   form_d(0);
 #ifdef S3_TIMING
@@ -481,39 +481,39 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
 #endif
   unsigned tflag_next = a.tplain[0];  // raw byte: tested one tile later
   for (int j = 0; j < ntiles; ++j) {
-    const int b = j % NS;
+    const int b = j % 3;
     const bool tflag = tflag_next != 0u;
     if (j + 1 < ntiles) tflag_next = a.tplain[j + 1];
 #ifdef S3_TIMING
     tm_x = clock64();
 #endif
-    cp_async_wait_pending(NS - 3);  // tile j + 1 has landed; tiles j + 2 .. j + NS - 2 may be in flight
+    asm volatile("cp.async.wait_group 0;\n" ::);  // tile j + 1 has landed
     __syncthreads();
 #ifdef S3_TIMING
     tm_wait += clock64() - tm_x;
     tm_x = clock64();
 #endif
     if (fst) {
-      if (j + NS - 1 < ntiles) stage_fast(j + NS - 1, (j + NS - 1) % NS, rn);
+      if (j + 2 < ntiles) stage_fast(j + 2, (j + 2) % 3, rn);
       cp_async_commit();
 #ifdef S3_TIMING
       tm_stage += clock64() - tm_x;
       tm_x = clock64();
 #endif
-      load_rho(j + NS, rn);  // consumed next iteration: latency hidden by this tile's compute
+      load_rho(j + 3, rn);  // consumed next iteration: latency hidden by this tile's compute
 #ifdef S3_TIMING
       tm_rho += clock64() - tm_x;
       tm_x = clock64();
 #endif
     } else {
-      if (j + NS - 1 < ntiles) stage(j + NS - 1, (j + NS - 1) % NS);
+      if (j + 2 < ntiles) stage(j + 2, (j + 2) % 3);
       cp_async_commit();
     }
 #ifdef S3_TIMING
     tm_stage += clock64() - tm_x;
     tm_x = clock64();
 #endif
-    if (j + 1 < ntiles) form_d((j + 1) % NS);
+    if (j + 1 < ntiles) form_d((j + 1) % 3);
 #ifdef S3_TIMING
     tm_fd += clock64() - tm_x;
     tm_x = clock64();
@@ -635,6 +635,9 @@ __host__ __device__ __forceinline__ int s3_lanes(long long pairs, long long fill
   return 1;
 }
 
+// SF = 1: the one-lane-per-pair program compiled on its own (every split
+// expression a constant); SF = 0: S lanes per pair at run time (2, 4).
+template <int SF>
 __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
   extern __shared__ double sm_dyn[];
   const int b = blockIdx.x;
@@ -656,7 +659,7 @@ __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
   }
   // with score1 taking the |phi(r)| = 1 candidates, the few multi-phase ones
   // run at their own split (latency-bound: one pass per lane per tile)
-  const int S = a.skip_nl1 ? a.s_multi : (a.st ? a.st->S : a.S);
+  const int S = SF ? 1 : (a.skip_nl1 ? a.s_multi : (a.st ? a.st->S : a.S));
   // work items (candidate group x scenario slice) strided over the grid: the
   // device loop launches a fixed, occupancy-sized grid for every iteration
   // (skip_nl1: the |phi(r)| = 1 items run in score1_kernel)
@@ -664,11 +667,11 @@ __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
     // counter slot: global candidate-group index (every group range is a
     // whole number of nsl-slice items)
     if (w < gc[1])
-      s3_body<1, 0, 0>(a, S, w, gs[1], gs[2] - gs[1], R, sm_dyn, 0);
+      s3_body<1, 0, SF>(a, S, w, gs[1], gs[2] - gs[1], R, sm_dyn, 0);
     else if (w < gc[2])
-      s3_body<2, 0, 0>(a, S, w - gc[1], gs[2], gs[3] - gs[2], R, sm_dyn, gc[1] / a.nsl);
+      s3_body<2, 0, SF>(a, S, w - gc[1], gs[2], gs[3] - gs[2], R, sm_dyn, gc[1] / a.nsl);
     else
-      s3_body<3, 0, 0>(a, S, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
+      s3_body<3, 0, SF>(a, S, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
     __syncthreads();  // shared memory is reused by the next item
   }
 }
