@@ -789,6 +789,35 @@ struct Engine::Impl {
           }
         }
         B.walk = tree ? put4(wk) : -1;
+        if (tree && std::getenv("KRONRED_WALK_STATS")) {  // debugging aid: elimination-tree depth
+          std::vector<int> dep(size_t(nn), 0);
+          long long sum = 0;
+          int mx = 0, cnt = 0;
+          for (int st = h.nsteps - 1; st >= 0; --st) {
+            const int k = h.step_node[size_t(st)], par = wk[size_t(k) * 4 + 1];
+            dep[size_t(k)] = par >= 0 && wk[size_t(par) * 4] >= 0 ? dep[size_t(par)] + 1 : 1;
+            sum += dep[size_t(k)];
+            mx = std::max(mx, dep[size_t(k)]);
+            ++cnt;
+          }
+          std::fprintf(stderr, "walk: %d steps, depth mean %.1f max %d, levels %d\n", cnt, double(sum) / std::max(cnt, 1), mx, nbr);
+          const int lanes = int(brecs.size() / 4) / std::max(nbr + 1, 1);
+          for (int r = 0; r < nbr; ++r)
+            for (int l = 0; l < lanes; ++l) {
+              const size_t q = size_t(r * lanes + l) * 4;
+              if (brecs[q] < 0 || bext[q] == 0) continue;
+              std::fprintf(stderr, "  backward round %d lane %d: general mk %d couplings %d:", r, l, bext[q + 1], bext[q + 3]);
+              for (int e = 0; e < bext[q + 3]; ++e) std::fprintf(stderr, " mj%d", be2[size_t(bext[q + 2] + e) * 2] >> 24);
+              std::fprintf(stderr, "\n");
+            }
+          for (int st = 0; st < h.nsteps; ++st) {
+            const int k = h.step_node[size_t(st)];
+            const int q = frec_of_step[size_t(st)] * 4;
+            if (frecs[size_t(q) + 2] >= 0) continue;
+            std::fprintf(stderr, "  forward step %d node %d: general mk %d pulls %d depth %d\n", st, k, fext[size_t(q) + 1],
+                         fext[size_t(q) + 3], dep[size_t(k)]);
+          }
+        }
       }
       while (bm.size() % 4) bm.push_back(0);
       B.nfr = nfr;

@@ -506,6 +506,58 @@ __device__ __forceinline__ C2 cfl(unsigned cs, const double2* cf, int byteoff) {
   }
 }
 
+// General (multi-phase) backward step, m_k, m_j <= 3. Every operand is loaded up
+// front at a clamped (always in-block) index and the products are folded with
+// selects, so the loads issue back to back instead of one predicated
+// load -> product pair at a time; the folded operations and their order are
+// those of the reference's Mat3c/Vec3c loops (only c < m_j / r < m_k terms).
+__device__ __forceinline__ void gen_block_load(C2 (&A)[9], const double2* blk, int mr, int mc) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) A[r * 3 + c] = ld2(blk + min(r, mr - 1) * mc + min(c, mc - 1));
+}
+
+// backward: x_k = t_k - pinv_k (sum_j U_kj x_j) (solver.cpp:136-147)
+__device__ __forceinline__ void gen_bwd_step(const int4 rc, const int4 rx, double2* x, const double2* cf,
+                                             const int2* be) {
+  const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
+  C2 acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  for (int e = rx.z; e < rx.z + rx.w; ++e) {
+    const int2 en = be[e];
+    const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+    C2 xv[3], A[9];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) xv[c] = ld2(x + xj + min(c, mj - 1));
+    gen_block_load(A, cf + bo, mk, mj);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      C2 u = {0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const C2 t = dev::cadd(u, dev::cmul(A[r * 3 + c], xv[c]));
+        u = c < mj ? t : u;
+      }
+      const C2 t = dev::cadd(acc[r], u);
+      acc[r] = r < mk ? t : acc[r];
+    }
+  }
+  C2 P[9], xo[3];
+  gen_block_load(P, cf + po, mk, mk);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) xo[r] = ld2(x + xk + min(r, mk - 1));
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    C2 corr = {0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const C2 t = dev::cadd(corr, dev::cmul(P[r * 3 + c], acc[c]));
+      corr = c < mk ? t : corr;
+    }
+    if (r < mk) st2(x + xk + r, dev::csub(xo[r], corr));
+  }
+}
+
 // One forward elimination step of the lane-slot program (pull form): node k's
 // right-hand side minus its children's contributions in elimination order,
 // times pinv_k (solver.cpp:125-134; the scalar fast path and the general
@@ -686,33 +738,7 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
       }
       sts2(xs + rc.x, dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc))));
     } else if (rc.x >= 0) {
-      const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
-      C2 acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-      for (int e = rx.z; e < rx.z + rx.w; ++e) {
-        const int2 en = be[e];
-        const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
-        C2 xv[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) xv[c] = c < mj ? ld2(x + xj + c) : C2{0.0, 0.0};
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          if (r >= mk) continue;
-          C2 u = {0.0, 0.0};
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            if (c < mj) u = dev::cadd(u, dev::cmul(ld2(cf + bo + r * mj + c), xv[c]));
-          acc[r] = dev::cadd(acc[r], u);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        if (r >= mk) continue;
-        C2 corr = {0.0, 0.0};
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          if (c < mk) corr = dev::cadd(corr, dev::cmul(ld2(cf + po + r * mk + c), acc[c]));
-        st2(x + xk + r, dev::csub(ld2(x + xk + r), corr));
-      }
+      gen_bwd_step(rc, rx, x, cf, be);
     }
     aa = aa_n;
     pv = pv_n;
@@ -730,15 +756,30 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   // step with its single coupling): no vote, no extension records.
 #pragma unroll 2
   for (; br < nbr; ++br) {
+#ifdef BR_TRACE
+    if (tr_on && br < 80) {
+      tr_a[br] = __ballot_sync(0xffffffffu, rc.x >= 0);
+      tr_g[br] = 0;
+      tr_t[br] = clock64();
+    }
+#endif
     const C2 xj = lds2(xs + (rc.x >= 0 ? rc.z : 0));
     const bool scn = nx.x >= 0;
     const C2 aa_n = cfl<SM>(cs, cf, scn ? nx.w : 0), pv_n = cfl<SM>(cs, cf, scn ? nx.y : 0);
     const C2 t_n = lds2(xs + (scn ? nx.x : 0));
     const int4 nx2 = rec4<SM>(ssl, bsl, min(br + 2, nbr) * rstride);
-    if (rc.x >= 0) {
-      const C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj));
-      sts2(xs + rc.x, dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc))));
-    }
+    // computed on every lane (empty slots on zeros), stored on active ones:
+    // keeps the parent's load a straight-line first load, ahead of the next
+    // round's operand loads in the shared-memory queue
+#ifdef BR_TRACE
+    if (tr_on && br < 80 && xj.x != 1.2345e300) tr_b[br] = clock64();
+#endif
+    const C2 acc = dev::cadd(C2{0.0, 0.0}, dev::cmul(aa, xj));
+    const C2 res = dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc)));
+#ifdef BR_TRACE
+    if (tr_on && br < 80 && res.x != 1.2345e300) tr_c[br] = clock64();
+#endif
+    if (rc.x >= 0) sts2(xs + rc.x, res);
     aa = aa_n;
     pv = pv_n;
     t = t_n;
@@ -933,6 +974,7 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
   if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 9] = globaltimer_ns();
   tree_backward<SM>(a, M, xs, cs, x, cf, lane, WB, WB > 1 ? warp : 0);
   if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[3] = clock64();
+  if (a.tdbg && blockIdx.x == 0 && tid == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 11] = globaltimer_ns();
   for (int r = WB > 1 ? tid : lane; r < a.nphi; r += 32 * WB) a.bv[bv_base(size_t(r), a.L, rhs)] = x[r];
   if (a.tdbg && blockIdx.x == 0 && tid == 0) {
     unsigned long long t;
