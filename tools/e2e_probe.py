@@ -1,0 +1,20 @@
+"""Breakdown of the e2e call (bench.py e2e leg): reload from host, the
+reduction (host wall vs device time), result read-back."""
+import sys, time
+from pathlib import Path
+ROOT = Path(__file__).resolve().parents[1]
+sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
+import torch
+import paper_2510_19608_b200 as kr
+from golden_io import path
+case = sys.argv[1] if len(sys.argv) > 1 else "c2"
+hp = kr.HostProblem(str(path(case, "net.json")), str(path(case, "scen.csv")))
+ctx = kr.Context(hp, device=0)
+cfg = kr.ReductionConfig(e_bar=3e-3)
+ctx.run_reduction(cfg)
+for rep in range(4):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter(); ctx.reload(hp); torch.cuda.synchronize(); t1 = time.perf_counter()
+    r = ctx.run_reduction(cfg); t2 = time.perf_counter()
+    m = r.model; torch.cuda.synchronize(); t3 = time.perf_counter()
+    print(f"reload {1e3*(t1-t0):.2f} ms | run wall {1e3*(t2-t1):.2f} ms (device {r.device_ms:.2f}) | model {1e3*(t3-t2):.2f} ms")
