@@ -1929,27 +1929,13 @@ struct Engine::Impl {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occc, score_kernel<true>, threadsc, smemc));
         gridc = std::max(1, std::min((2 * nb + qc.G) / qc.G, std::max(1, occc) * sms));
       }
-      // Scorer start without the refresh edge (rwait): the next iteration's
-      // scorer depends on the enumeration only and waits on the device for
-      // the refresh's arrivals (wait_base_refresh), so its launch latency
-      // overlaps the refresh. The chains alternate between the two streams:
-      // copy u scores, picks and refreshes on sx, enumerates on sy, and copy
-      // u + 1 scores on sy (after the enumeration) and joins sx's refresh
-      // before its pick. The refresh grid must be resident at once (it is
-      // launched first; a spinning scorer never holds back its CTAs).
-      const dim3 rg((L + bb.W - 1) / bb.W), rb(32 * bb.W * bb.WB);
-      const bool rwait = !cplx && int(rg.x) <= sms && std::getenv("KRONRED_NO_RWAIT") == nullptr;
-      lb.ref_cta = rwait ? int(rg.x) : 0;
-      q.ref_wait = rwait ? 1 : 0;
-      bb.signal = rwait ? 1 : 0;
-      cudaStream_t sx = stream, sy = stream2;
       for (int u = 0; u < kLoopUnroll; ++u) {
       if (cplx) {
-        score_kernel<true><<<gridc, threadsc, smemc, sx>>>(qc);
+        score_kernel<true><<<gridc, threadsc, smemc, stream>>>(qc);
       } else if (s1) {
         // |phi(r)| >= 2 candidates (score3) next to the |phi(r)| = 1 ones
         // (score1<S>, S picked by the enumeration through a switch node)
-        CK(cudaEventRecord(ev_fork3, sx));
+        CK(cudaEventRecord(ev_fork3, stream));
         CK(cudaStreamWaitEvent(stream3, ev_fork3, 0));
         {
           // the multi-phase items are few and latency-bound (each walks every
@@ -1970,17 +1956,17 @@ struct Engine::Impl {
           CK(cudaLaunchKernelEx(&lc, score3_kernel<0>, q));
         }
         lb.scond = hsw[(u + 1) % kLoopUnroll];  // set by this copy's enumeration
-        add_switch(sx, hsw[u], [&](int i, cudaStream_t cs) {
+        add_switch(stream, hsw[u], [&](int i, cudaStream_t cs) {
           const int Si = i == 0 ? 1 : (i == 1 ? 2 : 4);
           launch_s1(Si, q, s1_grid(Si, items_max), cs);
         });
         CK(cudaEventRecord(ev_join3, stream3));
-        CK(cudaStreamWaitEvent(sx, ev_join3, 0));
+        CK(cudaStreamWaitEvent(stream, ev_join3, 0));
       } else {
         // every candidate in score3: the split picks the compiled S = 1 kernel
         // or the run-time split one
         lb.scond = hsw[(u + 1) % kLoopUnroll];
-        add_switch(sx, hsw[u], [&](int i, cudaStream_t cs) {
+        add_switch(stream, hsw[u], [&](int i, cudaStream_t cs) {
           if (i == 0)
             score3_kernel<1><<<grid3, s3_threads(), sm3, cs>>>(q);
           else
@@ -1989,36 +1975,20 @@ struct Engine::Impl {
           CK(cudaGetLastError());
         });
       }
-      if (rwait && u > 0) {  // the previous copy's refresh (long done: the scores waited on it)
-        CK(cudaEventRecord(ev_join, sy));
-        CK(cudaStreamWaitEvent(sx, ev_join, 0));
-      }
       // pick and refresh follow their stream predecessor by programmatic
       // dependent launch (launch overlapped with the predecessor's tail; each
       // waits on griddepcontrol before reading its results)
-      launch_dep(pdl && !s1 && !cplx && !(rwait && u > 0), pick_commit_kernel, dim3(1), dim3(kLoopThreads), 0, sx,
-                 lb);
-      CK(cudaEventRecord(ev_fork, sx));
-      CK(cudaStreamWaitEvent(sy, ev_fork, 0));
-      enum_kernel<<<1, kLoopThreads, enum_smem(), sy>>>(lb);
+      launch_dep(pdl && !s1 && !cplx, pick_commit_kernel, dim3(1), dim3(kLoopThreads), 0, stream, lb);
+      CK(cudaEventRecord(ev_fork, stream));
+      CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
+      enum_kernel<<<1, kLoopThreads, enum_smem(), stream2>>>(lb);
+      const dim3 rg((L + bb.W - 1) / bb.W), rb(32 * bb.W * bb.WB);
       if (full.bsm)
-        launch_dep(pdl, base_refresh_kernel<true>, rg, rb, size_t(full.bsmem), sx, bb);
+        launch_dep(pdl, base_refresh_kernel<true>, rg, rb, size_t(full.bsmem), stream, bb);
       else
-        launch_dep(pdl, base_refresh_kernel<false>, rg, rb, size_t(full.bsmem), sx, bb);
-      if (rwait) {
-        std::swap(sx, sy);  // the next copy scores after the enumeration
-      } else {
-        CK(cudaEventRecord(ev_join, sy));
-        CK(cudaStreamWaitEvent(sx, ev_join, 0));
-      }
-      }
-      if (sx != stream) {  // join the other chain back into the capture origin
-        CK(cudaEventRecord(ev_join, sx));
-        CK(cudaStreamWaitEvent(stream, ev_join, 0));
-      }
-      if (rwait) {
-        CK(cudaEventRecord(ev_join, stream2));
-        CK(cudaStreamWaitEvent(stream, ev_join, 0));
+        launch_dep(pdl, base_refresh_kernel<false>, rg, rb, size_t(full.bsmem), stream, bb);
+      CK(cudaEventRecord(ev_join, stream2));
+      CK(cudaStreamWaitEvent(stream, ev_join, 0));
       }
       CK(cudaStreamEndCapture(stream, &body));
       CK(cudaGraphInstantiate(&loop_exec, graph, 0));

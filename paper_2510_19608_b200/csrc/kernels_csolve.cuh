@@ -50,26 +50,7 @@ struct LoopState {
   int last_s, last_r;  // the last committed candidate (incremental base refresh)
   int grp_start[4];  // candidate offset of each |phi(r)| group (index 1..3)
   int grp_cta[4];    // first CTA of each group; grp_cta[3] = CTAs in use
-  // scorer start on the base refresh (device loop, no graph edge): the pick
-  // raises the target by the refresh grid per commit, every refresh CTA
-  // arrives once when its base columns are written
-  unsigned ref_target, ref_arrive;
 };
-
-// Scorer side: one thread waits (acquire) until the last commit's base
-// refresh has arrived on every CTA, the CTA's barrier passes it on.
-__device__ __forceinline__ void wait_base_refresh(const LoopState* st) {
-  if (threadIdx.x == 0) {
-    const unsigned target = st->ref_target;
-    unsigned v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&st->ref_arrive) : "memory");
-      if (v >= target) break;
-      __nanosleep(32);
-    }
-  }
-  __syncthreads();
-}
 
 // offsets (in ints) of the packed program sections
 struct CProg {
@@ -436,7 +417,6 @@ struct BaseArgs {
   int inc_s, inc_r;       // changed nodes (host-driven loop)
   int walk;               // ints offset in M of [node] int4 {record, parent, step, 0} (-1 record: kept)
   int rhs_staged;         // incremental: right-hand sides staged in a second buffer per warp
-  int signal;             // device loop: arrive on st->ref_arrive when the base columns are written
 };
 
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
@@ -1002,18 +982,6 @@ __global__ void __launch_bounds__(256) base_refresh_kernel(BaseArgs a) {
     a.tdbg[size_t(a.st->iter) * kTdbg + 5] = t;
   }
   if (a.tdbg && lane == 0) atomicMax(a.tdbg + size_t(a.st->iter) * kTdbg + 10, globaltimer_ns());
-  if (a.signal) {
-    __syncthreads();  // every warp's base columns (exited warps count as arrived)
-    if (tid == 0) {
-      if (a.tdbg) {  // timeline: when the release completes (the fetch returns)
-        unsigned old;
-        asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(&a.st->ref_arrive) : "memory");
-        atomicMax(a.tdbg + size_t(a.st->iter) * kTdbg + 13, globaltimer_ns() + (old & 0u));
-      } else {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.st->ref_arrive) : "memory");
-      }
-    }
-  }
 }
 
 // cfac[i] = (src >= 0 ? (src & 1 ? pinv : blocks)[src >> 1] : 0)

@@ -35,7 +35,6 @@ struct LoopArgs {
   int s_multi;         // score3's split for the |phi(r)| >= 2 groups when score1 runs
   long long fill;      // scorer row split: thread budget (s3_lanes)
   int force_s;         // scorer row split forced to 1/2/4 (0: automatic)
-  int ref_cta;         // > 0: the scorer waits on st->ref_arrive; the refresh grid (pick raises the target)
   int inc_enum;        // 1: incremental candidate list after a commit (else full rebuild)
   int kcap;            // keys region size (power of two >= 2 nb); the previous list follows it
   int nsl;             // scenario slices per candidate group (score3), 1 otherwise
@@ -812,7 +811,6 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
     st->last_r = r;
     if (a.has_target && double(a.n - (ns - 1)) / double(a.n) >= a.target) st->done = 1;
     if (it + 1 >= a.cap) st->done = 1;
-    if (a.ref_cta && !st->done) st->ref_target += unsigned(a.ref_cta);  // this commit's base refresh
     if (a.tdbg) a.tdbg[size_t(it) * kTdbg + 1] = globaltimer();
     if (a.live_count && it < a.cap) {
       // every thread's row stores precede the barriers above; make them

@@ -311,7 +311,6 @@ __global__ void __launch_bounds__(S1Geom<S, GK>::P, s1_min_blocks(S1Geom<S, GK>:
   int R = a.R, n1 = a.grp_start[2] - a.grp_start[1], items = a.grp_cta[1];
   if (a.st) {
     if (a.st->done) return;
-    if (a.ref_wait) wait_base_refresh(a.st);
     R = a.st->R;
     n1 = a.st->grp_start[2] - a.st->grp_start[1];
     items = a.st->grp_cta[1];

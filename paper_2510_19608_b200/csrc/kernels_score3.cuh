@@ -47,7 +47,6 @@ struct S3Args {
   int S;                     // lanes per pair (host-driven loop; the device loop reads st->S)
   int skip_nl1;              // 1: leave the |phi(r)| = 1 items to score1_kernel
   int s_multi;               // lanes per pair of the |phi(r)| >= 2 items when skip_nl1
-  int ref_wait;              // device loop: wait for the base refresh on st (wait_base_refresh)
   int Ls, nsl;               // scenario slice width and slice count
   const int4* cand;          // grouped by |phi(r)|: (s, r, table row of s, table row of r)
   const int* cand_idx;       // lexicographic index of each grouped slot
@@ -648,10 +647,6 @@ __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
   const int* gc = a.grp_cta;
   if (a.st) {
     if (a.st->done) return;
-    const long long wc0 = clock64();
-    if (a.tdbg && b == 0 && threadIdx.x == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 12] = globaltimer_ns();
-    if (a.ref_wait) wait_base_refresh(a.st);
-    if (a.tdbg && b == 0 && threadIdx.x == 0) a.tdbg[size_t(a.st->iter) * kTdbg + 14] = clock64() - wc0;
     if (a.tdbg && b == 0 && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -50,8 +50,8 @@ for i in range(1, it - 1):
     ns = res.trace[i].supernode_count + 1  # before the commit
     # next iteration's enum / refresh phases, relative to this pick's end
     en = (nx[3] - c[1]) / 1e3
-    rs, rst, rwk, rbw, re0, rel, sen, rar = [(nx[k] - c[1]) / 1e3 for k in (4, 8, 9, 11, 5, 10, 12, 13)]
-    rows.append((i, C, ns, score, pick, after, en, rs, rst, rwk, re0, rel, rbw, sen, rar))
+    rs, rst, rwk, rbw, re0, rel = [(nx[k] - c[1]) / 1e3 for k in (4, 8, 9, 11, 5, 10)]
+    rows.append((i, C, ns, score, pick, after, en, rs, rst, rwk, re0, rel, rbw))
 a = np.array(rows)
 print(f"{args.case}: {it} iterations, L={L}, total device {res.device_ms:.1f} ms")
 print(" iters      C_avg   ns_avg  score_us  pick_us  enum|refresh_us  Mpair-rows/us")
@@ -63,10 +63,7 @@ for b0 in range(0, len(a), args.bucket):
 print(f"sum: score {a[:,3].sum()/1e3:.1f} ms, pick {a[:,4].sum()/1e3:.1f} ms, enum|refresh {a[:,5].sum()/1e3:.1f} ms")
 m = a[:, 6:].mean(axis=0)
 print(f"after pick (us, mean): enum end {m[0]:.1f} | refresh start {m[1]:.1f}, staged {m[2]:.1f}, "
-      f"walk done {m[3]:.1f}, backward done {m[6]:.1f}, CTA0 end {m[4]:.1f}, last CTA end {m[5]:.1f}, arrived {m[8]:.1f} | next scorer entry {m[7]:.1f}, score {a[:,5].mean():.1f}")
-wc = T[2:it, 14].astype(np.float64) / 1965.0
-a = np.column_stack([a, wc[:len(a)]]) if len(wc) >= len(a) else a
-print(f"scorer CTA0 wait (clock64): mean {wc.mean():.2f} us, median {np.median(wc):.2f} us")
+      f"walk done {m[3]:.1f}, backward done {m[6]:.1f}, CTA0 end {m[4]:.1f}, last CTA end {m[5]:.1f} | next score {a[:,5].mean():.1f}")
 if args.out:
     np.savetxt(args.out, a, fmt="%.3f", delimiter="\t",
-               header="iter\tC\tns\tscore_us\tpick_us\tafter_us\tenum_end\tref_start\tref_staged\tref_walk\tref_end0\tref_end\tref_bwd\tscore_entry\tref_arrived\twait_us")
+               header="iter\tC\tns\tscore_us\tpick_us\tafter_us\tenum_end\tref_start\tref_staged\tref_walk\tref_end0\tref_end\tref_bwd")
