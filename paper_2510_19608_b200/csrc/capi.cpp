@@ -208,12 +208,23 @@ void fill_views(krg_host_problem& hp) {
 }
 
 Problem base_problem(const Network& net) {
+  const bool tr = std::getenv("KRONRED_RELOAD_TRACE") != nullptr;  // tuning aid: phase times
+  const auto t0 = std::chrono::steady_clock::now();
   validate_or_throw(net);
+  const auto t1 = std::chrono::steady_clock::now();
   Problem p;
   p.net = net;
   for (const Node& nd : net.nodes) p.mask.push_back(nd.phases.bits);
   p.slack = net.slack_id();
-  p.y = FlatBlocks::from(assemble_admittance(net));
+  const auto t2 = std::chrono::steady_clock::now();
+  const BlockAdmittance y = assemble_admittance(net);
+  const auto t3 = std::chrono::steady_clock::now();
+  p.y = FlatBlocks::from(y);
+  if (tr) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "assembly: validate %.3f ms, copy %.3f ms, admittance %.3f ms, flatten %.3f ms\n", ms(t0, t1),
+                 ms(t1, t2), ms(t2, t3), ms(t3, std::chrono::steady_clock::now()));
+  }
   return p;
 }
 
@@ -230,35 +241,57 @@ void zero_invalid(const Network& net, std::vector<double>& inj, int L) {
 }
 
 // scenario_consistent (scenario.cpp:26-31): residual of Y V = I on non-slack
-// present-phase rows, relative to max(1, |I|_inf).
+// present-phase rows, relative to max(1, |I|_inf). Scenarios are independent:
+// they are checked on up to 16 host threads, and the first failing one (in
+// library order) is reported, as the sequential loop would.
 void check_residual(const Problem& p, const std::vector<double>& inj, const std::vector<double>& volt,
                     const std::vector<std::string>& ids) {
   const int n = p.y.n;
-  for (size_t l = 0; l < ids.size(); ++l) {
-    const double* V = volt.data() + l * size_t(6 * n);
-    const double* I = inj.data() + l * size_t(6 * n);
+  const size_t L = ids.size();
+  // std::complex product without the C99 Annex G call for finite operands
+  // (same bits; NaN results take the library path)
+  auto mul = [](cx a, cx b) {
+    const double re = a.real() * b.real() - a.imag() * b.imag(), im = a.real() * b.imag() + a.imag() * b.real();
+    return (std::isnan(re) && std::isnan(im)) ? a * b : cx{re, im};
+  };
+  std::vector<char> ok(L, 1);
+  auto check = [&](size_t l0, size_t l1) {
     std::vector<cx> yv(size_t(3 * n));
-    for (size_t b = 0; b < p.y.row.size(); ++b) {
-      const int i = p.y.row[b], j = p.y.col[b];
-      for (int r = 0; r < 3; ++r) {
-        cx acc{};
-        for (int c = 0; c < 3; ++c)
-          acc += cx{p.y.val[b * 18 + size_t(6 * r + 2 * c)], p.y.val[b * 18 + size_t(6 * r + 2 * c + 1)]} *
-                 cx{V[(3 * j + c) * 2], V[(3 * j + c) * 2 + 1]};
-        yv[size_t(3 * i + r)] += acc;
+    for (size_t l = l0; l < l1; ++l) {
+      const double* V = volt.data() + l * size_t(6 * n);
+      const double* I = inj.data() + l * size_t(6 * n);
+      std::fill(yv.begin(), yv.end(), cx{});
+      for (size_t b = 0; b < p.y.row.size(); ++b) {
+        const int i = p.y.row[b], j = p.y.col[b];
+        const double* blk = p.y.val.data() + b * 18;
+        for (int r = 0; r < 3; ++r) {
+          cx acc{};
+          for (int c = 0; c < 3; ++c)
+            acc += mul(cx{blk[6 * r + 2 * c], blk[6 * r + 2 * c + 1]}, cx{V[(3 * j + c) * 2], V[(3 * j + c) * 2 + 1]});
+          yv[size_t(3 * i + r)] += acc;
+        }
       }
+      double res = 0, inorm = 0;
+      for (int k = 0; k < 3 * n; ++k) inorm = std::max(inorm, std::abs(cx{I[2 * k], I[2 * k + 1]}));
+      for (int i = 0; i < n; ++i) {
+        if (i == p.slack) continue;
+        for (int q = 0; q < 3; ++q)
+          if ((p.mask[size_t(i)] >> q) & 1)
+            res = std::max(res, std::abs(yv[size_t(3 * i + q)] - cx{I[(3 * i + q) * 2], I[(3 * i + q) * 2 + 1]}));
+      }
+      ok[l] = res <= 1e-10 * std::max(1.0, inorm) ? 1 : 0;
     }
-    double res = 0, inorm = 0;
-    for (int k = 0; k < 3 * n; ++k) inorm = std::max(inorm, std::abs(cx{I[2 * k], I[2 * k + 1]}));
-    for (int i = 0; i < n; ++i) {
-      if (i == p.slack) continue;
-      for (int q = 0; q < 3; ++q)
-        if ((p.mask[size_t(i)] >> q) & 1)
-          res = std::max(res, std::abs(yv[size_t(3 * i + q)] - cx{I[(3 * i + q) * 2], I[(3 * i + q) * 2 + 1]}));
-    }
-    if (!(res <= 1e-10 * std::max(1.0, inorm)))
-      throw SolverError("scenario '" + ids[l] + "' failed the residual check");
+  };
+  const size_t nt = std::min<size_t>(L, std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())));
+  if (nt <= 1 || size_t(n) * L < 4096) {
+    check(0, L);
+  } else {
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < nt; ++t) th.emplace_back(check, L * t / nt, L * (t + 1) / nt);
+    for (auto& t : th) t.join();
   }
+  for (size_t l = 0; l < L; ++l)
+    if (!ok[l]) throw SolverError("scenario '" + ids[l] + "' failed the residual check");
 }
 
 // Engine over a host problem: current mode solves V-hat, PQ mode runs the
@@ -291,8 +324,15 @@ void load_scenarios_from_host(Engine* eng, const Problem& p, const krg_host_prob
     zero_invalid(hp.net, inj, L);
     eng->set_scenarios(hp.ids, inj, {});
     volt.resize(inj.size());
+    const auto t0 = std::chrono::steady_clock::now();
     eng->scenario_voltages(volt.data());
+    const auto t1 = std::chrono::steady_clock::now();
     check_residual(p, inj, volt, hp.ids);
+    if (std::getenv("KRONRED_RELOAD_TRACE")) {
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "scenarios: V-hat %.3f ms, residual %.3f ms\n", ms(t0, t1),
+                   ms(t1, std::chrono::steady_clock::now()));
+    }
     return;
   }
   check_residual(p, inj, volt, hp.ids);

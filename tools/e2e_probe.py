@@ -7,12 +7,15 @@ sys.path[:0] = [str(ROOT), str(ROOT / "tests")]
 import torch
 import paper_2510_19608_b200 as kr
 from golden_io import path
-case = sys.argv[1] if len(sys.argv) > 1 else "c2"
+case = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "c2"
 hp = kr.HostProblem(str(path(case, "net.json")), str(path(case, "scen.csv")))
 ctx = kr.Context(hp, device=0)
 cfg = kr.ReductionConfig(e_bar=3e-3)
 ctx.run_reduction(cfg)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda:0") if "--flush" in sys.argv else None
 for rep in range(4):
+    if flush is not None:
+        flush.zero_()
     torch.cuda.synchronize()
     t0 = time.perf_counter(); ctx.reload(hp); torch.cuda.synchronize(); t1 = time.perf_counter()
     r = ctx.run_reduction(cfg); t2 = time.perf_counter()
