@@ -287,7 +287,7 @@ def main() -> None:
         m = r2.model
         torch.cuda.synchronize()
         e2e_ms.append(max_over_ranks(1e3 * (time.perf_counter() - t0)))
-        d2h = len(r2.trace) * (8 * 4 + 8 * L) + len(m.y_kron) * 144 + len(m.kept_ids) * 5 + 8 * L
+        d2h = len(r2.trace_arrays["s"]) * (8 * 4 + 8 * L) + len(m.y_kron) * 144 + len(m.kept_ids) * 5 + 8 * L
     del c2
     e2e_value = cands / (statistics.mean(e2e_ms) / 1e3)
 

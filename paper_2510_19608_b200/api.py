@@ -393,11 +393,22 @@ class Result:
         _check(L.krg_result_trace(handle, _p(s, C.c_int32), _p(r, C.c_int32), _p(sm, C.c_double),
                                   _p(me, C.c_double), _p(snc, C.c_int32), _p(cc, C.c_int32), _p(wall, C.c_double)))
         me = me[: it * ns].reshape(it, ns) if ns else np.zeros((it, 0))
-        self.trace = [TraceRow(i + 1, int(s[i]), int(r[i]), float(sm[i]), me[i], int(snc[i]), int(cc[i]),
-                               float(wall[i])) for i in range(it)]
+        # the trace arrives as arrays; the per-row objects are built on first access
+        self.trace_arrays = {"s": s[:it], "r": r[:it], "smice": sm[:it], "max_err": me, "supernode_count": snc[:it],
+                             "candidate_count": cc[:it], "wall_ms": wall[:it]}
+        self._trace = None
         self.total_candidates = int(L.krg_result_total_candidates(handle))
         self.device_ms = float(L.krg_result_device_ms(handle))
         self.model = self._model()
+
+    @property
+    def trace(self) -> list:
+        if self._trace is None:
+            t = self.trace_arrays
+            self._trace = [TraceRow(i + 1, int(t["s"][i]), int(t["r"][i]), float(t["smice"][i]), t["max_err"][i],
+                                    int(t["supernode_count"][i]), int(t["candidate_count"][i]), float(t["wall_ms"][i]))
+                           for i in range(len(t["s"]))]
+        return self._trace
 
     def _model(self) -> ReducedModel:
         L = lib()

@@ -308,7 +308,9 @@ std::unique_ptr<Engine> engine_from_host(const krg_host_problem& hp, int device)
 void load_scenarios_from_host(Engine* eng, const Problem& p, const krg_host_problem& hp) {
   const int L = int(hp.ids.size());
   if (L == 0) return;
-  std::vector<double> inj, volt;
+  // per-thread scratch, reused across calls (MB-sized fresh vectors cost
+  // their page faults on every reload)
+  thread_local std::vector<double> inj, volt;
   if (hp.pq) {
     for (size_t g = 0; g < hp.ids.size(); ++g)
       for (const auto& ld : hp.pq_loads[g])
@@ -320,7 +322,7 @@ void load_scenarios_from_host(Engine* eng, const Problem& p, const krg_host_prob
     eng->pq_to_currents(hp.pq_loads, inj, volt);
   } else {
     // current mode: V-hat = solve(I-hat) on the device (the engine keeps both)
-    inj = hp.inj;
+    inj.assign(hp.inj.begin(), hp.inj.end());
     zero_invalid(hp.net, inj, L);
     eng->set_scenarios(hp.ids, inj, {});
     volt.resize(inj.size());

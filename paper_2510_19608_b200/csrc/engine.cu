@@ -1186,6 +1186,36 @@ struct Engine::Impl {
 
   // ScenarioLibrary on the device (load_library: V-hat = solve(I-hat) when
   // the voltages are not given, scenario.cpp:39-50).
+  // Host <-> device copies of the per-call inputs and results (reload, the
+  // scenario library) through one pinned staging buffer kept by the engine:
+  // a memcpy into pinned memory plus an async DMA beats a pageable copy
+  // (driver bounce buffers) for these 0.1-2 MB transfers.
+  char* h_stage = nullptr;
+  size_t h_stage_cap = 0;
+  char* stage_buf(size_t bytes) {
+    if (h_stage_cap < bytes) {
+      if (h_stage) CK(cudaFreeHost(h_stage));
+      h_stage = nullptr;
+      CK(cudaMallocHost(reinterpret_cast<void**>(&h_stage), bytes));
+      h_stage_cap = bytes;
+    }
+    return h_stage;
+  }
+  void h2d_staged(void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    char* p = stage_buf(bytes);
+    CK(cudaStreamSynchronize(stream));  // the buffer's previous transfer is done
+    std::memcpy(p, src, bytes);
+    CK(cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, stream));
+  }
+  void d2h_staged(void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    char* p = stage_buf(bytes);
+    CK(cudaMemcpyAsync(p, src, bytes, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    std::memcpy(dst, p, bytes);
+  }
+
   void load_scenarios(const std::vector<std::string>& ids, const std::vector<double>& inj,
                       const std::vector<double>& volt) {
     if (comm && (24 + 8 * int(ids.size()) + 15) / 16 * 16 > rec_bytes)
@@ -1197,16 +1227,16 @@ struct Engine::Impl {
     prob.voltages = volt;
     if (L == 0) return;
     d_inj.alloc(size_t(L) * 3 * n);
-    CK(cudaMemcpy(d_inj.p, inj.data(), inj.size() * sizeof(double), cudaMemcpyHostToDevice));
+    h2d_staged(d_inj.p, inj.data(), inj.size() * sizeof(double));
     d_vhat.alloc(size_t(L) * 3 * n);
     if (!volt.empty()) {
+      CK(cudaStreamSynchronize(stream));  // (one staging buffer)
       CK(cudaMemcpy(d_vhat.p, volt.data(), volt.size() * sizeof(double), cudaMemcpyHostToDevice));
       h_vhat = volt;
     } else {
       solve_full(full, d_slackv.p, d_inj.p, L, d_vhat.p);
       h_vhat.resize(size_t(L) * 6 * n);
-      CK(cudaMemcpyAsync(h_vhat.data(), d_vhat.p, h_vhat.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
+      d2h_staged(h_vhat.data(), d_vhat.p, h_vhat.size() * sizeof(double));
       prob.voltages = h_vhat;
     }
     d_vhatp.alloc(size_t(nphi) * L);
@@ -1236,6 +1266,7 @@ struct Engine::Impl {
       cudaEventDestroy(ev_run1);
     }
     if (h_best) cudaFreeHost(h_best);
+    if (h_stage) cudaFreeHost(h_stage);
     if (h_fail) cudaFreeHost(h_fail);
     if (h_loopst) cudaFreeHost(h_loopst);
     if (h_trace) cudaFreeHost(h_trace);
@@ -2229,8 +2260,7 @@ void Engine::reload(const Problem& p) {
   I.prob = p;
   I.prob.scenario_ids = ids;
   I.prob.L = I.L;
-  if (!p.y.val.empty())
-    CK(cudaMemcpyAsync(I.d_yin.p, p.y.val.data(), p.y.val.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
+  I.h2d_staged(I.d_yin.p, p.y.val.data(), p.y.val.size() * sizeof(double));
   double sv[6];
   for (int q = 0; q < 3; ++q) {
     sv[2 * q] = p.net.nodes[size_t(p.slack)].slack_voltage[q].real();
@@ -2401,6 +2431,7 @@ void Engine::zcols(double* out, std::int64_t cap) {
 
 void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& out) {
   Impl& I = *impl_;
+  const auto tw0 = std::chrono::steady_clock::now();
   out = ResultData{};
   out.L = I.L;
   I.ensure_events();
@@ -2506,6 +2537,9 @@ void Engine::run(const ReductionConfig& cfg, const Observer& obs, ResultData& ou
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, I.ev_run0, I.ev_run1));
   out.device_ms = ms;
+  if (std::getenv("KRONRED_RELOAD_TRACE"))
+    std::fprintf(stderr, "run: host wall %.3f ms, device %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw0).count(), double(ms));
 }
 
 void Engine::kron(const std::vector<int>& reduce, ReducedModel& model) {
