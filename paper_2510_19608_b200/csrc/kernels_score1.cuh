@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(S1Geom<S, GK>::P, s1_min_blocks(S1Geom<S, GK>:
     s1_item<S, GK>(a, w, n1, R, sm_dyn);
     __syncthreads();  // shared memory is reused by the next item
   }
+  if (a.tdbg && a.st && threadIdx.x == 0) atomicMax(a.tdbg + size_t(a.st->iter) * kTdbg + 15, globaltimer_ns());
 }
 
 }  // namespace

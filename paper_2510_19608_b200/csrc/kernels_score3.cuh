@@ -674,6 +674,7 @@ __global__ void __launch_bounds__(128, S3_MIN_BLOCKS) score3_kernel(S3Args a) {
       s3_body<3, 0, SF>(a, S, w - gc[2], gs[3], C - gs[3], R, sm_dyn, gc[2] / a.nsl);
     __syncthreads();  // shared memory is reused by the next item
   }
+  if (a.tdbg && a.st && threadIdx.x == 0) atomicMax(a.tdbg + size_t(a.st->iter) * kTdbg + 14, globaltimer_ns());
 }
 
 }  // namespace

@@ -64,6 +64,13 @@ print(f"sum: score {a[:,3].sum()/1e3:.1f} ms, pick {a[:,4].sum()/1e3:.1f} ms, en
 m = a[:, 6:].mean(axis=0)
 print(f"after pick (us, mean): enum end {m[0]:.1f} | refresh start {m[1]:.1f}, staged {m[2]:.1f}, "
       f"walk done {m[3]:.1f}, backward done {m[6]:.1f}, CTA0 end {m[4]:.1f}, last CTA end {m[5]:.1f} | next score {a[:,5].mean():.1f}")
+se = np.array([(T[i][0] - T[i][15]) / 1e3 for i in range(1, it - 1) if T[i][15] > 0])
+if len(se):
+    print(f"score1 last CTA end -> pick start: mean {se.mean():.2f} us, median {np.median(se):.2f} us")
+s3 = np.array([(T[i][0] - T[i][14]) / 1e3 for i in range(1, it - 1) if T[i][14] > 0])
+if len(s3):
+    print(f"score3 last CTA end -> pick start: mean {s3.mean():.2f} us, median {np.median(s3):.2f} us, "
+          f"score3 ends after score1 in {np.mean([T[i][14] > T[i][15] for i in range(1, it - 1)]) * 100:.0f} % of iterations")
 if args.out:
     np.savetxt(args.out, a, fmt="%.3f", delimiter="\t",
                header="iter\tC\tns\tscore_us\tpick_us\tafter_us\tenum_end\tref_start\tref_staged\tref_walk\tref_end0\tref_end\tref_bwd")
