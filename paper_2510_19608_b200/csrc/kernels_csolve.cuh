@@ -511,25 +511,32 @@ __device__ __forceinline__ C2 cfl(unsigned cs, const double2* cf, int byteoff) {
 // selects, so the loads issue back to back instead of one predicated
 // load -> product pair at a time; the folded operations and their order are
 // those of the reference's Mat3c/Vec3c loops (only c < m_j / r < m_k terms).
-__device__ __forceinline__ void gen_block_load(C2 (&A)[9], const double2* blk, int mr, int mc) {
+template <bool SM>
+__device__ __forceinline__ void gen_block_load(C2 (&A)[9], unsigned cs, const double2* cf, int blk, int mr, int mc) {
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) A[r * 3 + c] = ld2(blk + min(r, mr - 1) * mc + min(c, mc - 1));
+    for (int c = 0; c < 3; ++c) A[r * 3 + c] = cfl<SM>(cs, cf, (blk + min(r, mr - 1) * mc + min(c, mc - 1)) * 16);
 }
 
-// backward: x_k = t_k - pinv_k (sum_j U_kj x_j) (solver.cpp:136-147)
-__device__ __forceinline__ void gen_bwd_step(const int4 rc, const int4 rx, double2* x, const double2* cf,
-                                             const int2* be) {
+// backward: x_k = t_k - pinv_k (sum_j U_kj x_j) (solver.cpp:136-147). x in
+// shared memory (xs), the factor through cfl (shared or read-only global).
+template <bool SM>
+__device__ __forceinline__ void gen_bwd_step(const int4 rc, const int4 rx, unsigned xs, unsigned cs, double2* x,
+                                             const double2* cf, const int2* be) {
   const int xk = rc.x >> 4, mk = rx.y, po = rc.y >> 4;
   C2 acc[3] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  C2 P[9], xo[3];
+  gen_block_load<SM>(P, cs, cf, po, mk, mk);  // independent of the couplings: in flight first
+#pragma unroll
+  for (int r = 0; r < 3; ++r) xo[r] = lds2(xs + unsigned(xk + min(r, mk - 1)) * 16u);
   for (int e = rx.z; e < rx.z + rx.w; ++e) {
     const int2 en = be[e];
     const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
     C2 xv[3], A[9];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) xv[c] = ld2(x + xj + min(c, mj - 1));
-    gen_block_load(A, cf + bo, mk, mj);
+    for (int c = 0; c < 3; ++c) xv[c] = lds2(xs + unsigned(xj + min(c, mj - 1)) * 16u);
+    gen_block_load<SM>(A, cs, cf, bo, mk, mj);
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       C2 u = {0.0, 0.0};
@@ -542,10 +549,6 @@ __device__ __forceinline__ void gen_bwd_step(const int4 rc, const int4 rx, doubl
       acc[r] = r < mk ? t : acc[r];
     }
   }
-  C2 P[9], xo[3];
-  gen_block_load(P, cf + po, mk, mk);
-#pragma unroll
-  for (int r = 0; r < 3; ++r) xo[r] = ld2(x + xk + min(r, mk - 1));
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     C2 corr = {0.0, 0.0};
@@ -554,8 +557,9 @@ __device__ __forceinline__ void gen_bwd_step(const int4 rc, const int4 rx, doubl
       const C2 t = dev::cadd(corr, dev::cmul(P[r * 3 + c], acc[c]));
       corr = c < mk ? t : corr;
     }
-    if (r < mk) st2(x + xk + r, dev::csub(xo[r], corr));
+    if (r < mk) sts2(xs + unsigned(xk + r) * 16u, dev::csub(xo[r], corr));
   }
+  (void)x;
 }
 
 // One forward elimination step of the lane-slot program (pull form): node k's
@@ -738,7 +742,7 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
       }
       sts2(xs + rc.x, dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc))));
     } else if (rc.x >= 0) {
-      gen_bwd_step(rc, rx, x, cf, be);
+      gen_bwd_step<SM>(rc, rx, xs, cs, x, cf, be);
     }
     aa = aa_n;
     pv = pv_n;
