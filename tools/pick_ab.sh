@@ -1,3 +1,6 @@
-# pick/commit kernel changes: parity subset + the per-iteration timeline
-timeout 900 python -m pytest tests -m gpu -x -q -k "c2 or c1 or incremental or full_run or exchange or complex or live or m40" 2>&1 | tail -2
-timeout 300 python tools/iter_profile.py c2 --bucket 500 2>&1 | grep "after pick\|^sum\|total device\|pick start" | sort -u
+# pick inside the scorer's switch body: parity subset + A/B timeline against the last commit
+timeout 900 python -m pytest tests -m gpu -x -q -k "c2 or c1 or incremental or full_run or exchange or complex or live or m40 or large or h2k" 2>&1 | tail -2
+for v in new head new head; do
+  if [ $v = head ]; then export KRONRED_LIB=tools/_var_head/libkronred_b200.so; else unset KRONRED_LIB; fi
+  echo "== $v"; timeout 300 python tools/iter_profile.py c2 --bucket 500 2>&1 | grep "after pick\|^sum\|total device\|pick start" | sort -u
+done
