@@ -646,6 +646,9 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int C = st->C, c0 = st->c0, c1 = st->c0 + st->Cl;
   if (a.tdbg && tid == 0) a.tdbg[size_t(st->iter) * kTdbg + 0] = globaltimer();
+#ifdef PICK_CLK  // timing experiment: SM cycles per pick phase (CTA thread 0)
+  long long pk0 = clock64(), pk1 = 0, pk2 = 0, pk3 = 0;
+#endif
   // the commit's first reads (super-node map and active list, which only this
   // kernel writes) are issued ahead of the argmin
   const int sup0 = tid < a.n ? a.sup[tid] : -1;
@@ -655,6 +658,9 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
   int bi;
   unsigned bk;
   pick_block_argmin(a, c0, c1, ss, si, sk, bs, bi, bk);
+#ifdef PICK_CLK
+  pk1 = clock64();
+#endif
   const int L = a.L;
   const double* wme = nullptr;  // the winner's max_err[L] (its rank's record), else pmaxerr
   if (a.xch) {
@@ -746,6 +752,9 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
       a.live_t[it] = globaltimer();
     }
   }
+#ifdef PICK_CLK
+  pk2 = clock64();
+#endif
   // i_agg[s] += i_agg[r], i_agg[r] = 0 (reduce.cpp:336-343); bounds merge
   const unsigned ms = a.mask[s], mr = a.mask[r];
   const int rs0 = a.prow_off[s], rr0 = a.prow_off[r];
@@ -790,6 +799,9 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
       for (int i = r + 1 + tid; i <= s; i += kLoopThreads) a.mem_off[i] -= kr;
     (void)os0;
   }
+#ifdef PICK_CLK
+  pk3 = clock64();
+#endif
   // remove r from the ascending active list
   const int ns = st->ns;
   for (int k = tid; k < ns; k += kLoopThreads)
@@ -812,6 +824,12 @@ __global__ void __launch_bounds__(kLoopThreads) pick_commit_kernel(LoopArgs a) {
     if (a.has_target && double(a.n - (ns - 1)) / double(a.n) >= a.target) st->done = 1;
     if (it + 1 >= a.cap) st->done = 1;
     if (a.tdbg) a.tdbg[size_t(it) * kTdbg + 1] = globaltimer();
+#ifdef PICK_CLK
+    if (a.tdbg) {
+      const long long pk4 = clock64();
+      a.tdbg[size_t(it) * kTdbg + 12] = (unsigned long long)((pk1 - pk0) | ((pk2 - pk1) << 16) | ((pk3 - pk2) << 32) | ((pk4 - pk3) << 48));
+    }
+#endif
     if (a.live_count && it < a.cap) {
       // every thread's row stores precede the barriers above; make them
       // visible to the host before the count that publishes the row

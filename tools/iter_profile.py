@@ -71,6 +71,10 @@ s3 = np.array([(T[i][0] - T[i][14]) / 1e3 for i in range(1, it - 1) if T[i][14] 
 if len(s3):
     print(f"score3 last CTA end -> pick start: mean {s3.mean():.2f} us, median {np.median(s3):.2f} us, "
           f"score3 ends after score1 in {np.mean([T[i][14] > T[i][15] for i in range(1, it - 1)]) * 100:.0f} % of iterations")
+pk = T[2:it, 12]
+if pk.any():
+    f = lambda sh: np.median((pk >> sh) & 0xFFFF)
+    print("pick phases (SM cycles, median): argmin %d, trace %d, commit %d, active-list %d" % (f(0), f(16), f(32), f(48)))
 if args.out:
     np.savetxt(args.out, a, fmt="%.3f", delimiter="\t",
                header="iter\tC\tns\tscore_us\tpick_us\tafter_us\tenum_end\tref_start\tref_staged\tref_walk\tref_end0\tref_end\tref_bwd")
