@@ -659,61 +659,87 @@ struct Engine::Impl {
           recs.insert(recs.end(), {-1, 0, 0, 0});
           ext.insert(ext.end(), {0, 0, 0, 0});
         };
-        for (int lv = 0; lv < nl; ++lv) {
-          const int c0 = off[size_t(lv)], cnt = off[size_t(lv) + 1] - c0;
-          for (int r0 = 0; r0 < cnt; r0 += lanes, ++nrounds)
-            for (int ln = 0; ln < lanes; ++ln) {
-              if (r0 + ln >= cnt) {
-                empty();
-                continue;
-              }
-              const int st = steps[size_t(c0 + r0 + ln)];
-              const int k = h.step_node[size_t(st)];
-              const int mk = __builtin_popcount(h.mask[size_t(k)]);
-              if (fwd) frec_of_step[size_t(st)] = int(recs.size() / 4);
-              const int first = fwd ? fin_first[size_t(st)] : bcp_first[size_t(st)];
-              const int ne = fwd ? h.in_off[size_t(st) + 1] - h.in_off[size_t(st)]
-                                 : h.cpl_off[size_t(st) + 1] - h.cpl_off[size_t(st)];
-              const std::vector<int>& ex = fwd ? fin_x : bcp_x;
-              const std::vector<int>& eb = fwd ? fin_b : bcp_b;
-              bool scalar = mk == 1;
-              for (int e = 0; e < ne; ++e) scalar = scalar && (ex[size_t(first + e)] >> 24) == 1;
-              if (size_t(d.xoff[size_t(nn)]) * 16 >= (1u << 31) || size_t(g.size()) * 16 >= (1u << 31))
-                throw Error("base program offsets overflow");
-              if (scalar && fwd) {
-                // forward: the first two pulls inline; missing pulls are exact
-                // zero pulls (b - (0 + 0*x) == b bit for bit), so every scalar
-                // step runs the same instruction sequence with both products
-                // in flight at once
-                const int xj = ne == 0 ? d.xoff[size_t(k)] : (ex[size_t(first)] & 0xffffff);
-                const int bo = ne == 0 ? zero_cf : eb[size_t(first)];
-                const int xj1 = ne < 2 ? d.xoff[size_t(k)] : (ex[size_t(first + 1)] & 0xffffff);
-                const int bo1 = ne < 2 ? zero_cf : eb[size_t(first + 1)];
-                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, xj * 16, bo * 16});
-                ext.insert(ext.end(), {xj1 * 16, bo1 * 16, int(ents.size() / 2), std::max(ne - 2, 0)});
-                for (int e = 2; e < ne; ++e) {
-                  ents.push_back(ex[size_t(first + e)]);
-                  ents.push_back(eb[size_t(first + e)]);
-                }
-              } else if (scalar) {
-                // backward: first coupling inline (an exact-zero one when none)
-                const int xj = ne == 0 ? d.xoff[size_t(k)] : (ex[size_t(first)] & 0xffffff);
-                const int bo = ne == 0 ? zero_cf : eb[size_t(first)];
-                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, xj * 16, bo * 16});
-                ext.insert(ext.end(), {0, mk, int(ents.size() / 2), std::max(ne - 1, 0)});
-                for (int e = 1; e < ne; ++e) {
-                  ents.push_back(ex[size_t(first + e)]);
-                  ents.push_back(eb[size_t(first + e)]);
-                }
-              } else {
-                recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, fwd ? -1 : 0, 0});
-                ext.insert(ext.end(), {1, mk, int(ents.size() / 2), ne});
-                for (int e = 0; e < ne; ++e) {
-                  ents.push_back(ex[size_t(first + e)]);
-                  ents.push_back(eb[size_t(first + e)]);
-                }
+        // lanes a backward general step takes: one per present phase (its rows
+        // are independent until the pivot product, a shuffle apart) when the
+        // round is one warp and KRONRED_NO_GEN_SPLIT is unset
+        const bool split = !fwd && lanes == 32 && std::getenv("KRONRED_NO_GEN_SPLIT") == nullptr;
+        auto demand = [&](int st) {
+          if (!split) return 1;
+          const int k = h.step_node[size_t(st)];
+          const int mk = __builtin_popcount(h.mask[size_t(k)]);
+          const int first = bcp_first[size_t(st)];
+          const int ne = h.cpl_off[size_t(st) + 1] - h.cpl_off[size_t(st)];
+          bool scalar = mk == 1;
+          for (int e = 0; e < ne; ++e) scalar = scalar && (bcp_x[size_t(first + e)] >> 24) == 1;
+          return scalar ? 1 : mk;
+        };
+        int gen_first = 0;
+        auto emit = [&](int st, int row) {
+          const int k = h.step_node[size_t(st)];
+          const int mk = __builtin_popcount(h.mask[size_t(k)]);
+          if (fwd) frec_of_step[size_t(st)] = int(recs.size() / 4);
+          const int first = fwd ? fin_first[size_t(st)] : bcp_first[size_t(st)];
+          const int ne = fwd ? h.in_off[size_t(st) + 1] - h.in_off[size_t(st)]
+                             : h.cpl_off[size_t(st) + 1] - h.cpl_off[size_t(st)];
+          const std::vector<int>& ex = fwd ? fin_x : bcp_x;
+          const std::vector<int>& eb = fwd ? fin_b : bcp_b;
+          bool scalar = mk == 1;
+          for (int e = 0; e < ne; ++e) scalar = scalar && (ex[size_t(first + e)] >> 24) == 1;
+          if (size_t(d.xoff[size_t(nn)]) * 16 >= (1u << 31) || size_t(g.size()) * 16 >= (1u << 31))
+            throw Error("base program offsets overflow");
+          if (scalar && fwd) {
+            // forward: the first two pulls inline; missing pulls are exact
+            // zero pulls (b - (0 + 0*x) == b bit for bit), so every scalar
+            // step runs the same instruction sequence with both products
+            // in flight at once
+            const int xj = ne == 0 ? d.xoff[size_t(k)] : (ex[size_t(first)] & 0xffffff);
+            const int bo = ne == 0 ? zero_cf : eb[size_t(first)];
+            const int xj1 = ne < 2 ? d.xoff[size_t(k)] : (ex[size_t(first + 1)] & 0xffffff);
+            const int bo1 = ne < 2 ? zero_cf : eb[size_t(first + 1)];
+            recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, xj * 16, bo * 16});
+            ext.insert(ext.end(), {xj1 * 16, bo1 * 16, int(ents.size() / 2), std::max(ne - 2, 0)});
+            for (int e = 2; e < ne; ++e) {
+              ents.push_back(ex[size_t(first + e)]);
+              ents.push_back(eb[size_t(first + e)]);
+            }
+          } else if (scalar) {
+            // backward: first coupling inline (an exact-zero one when none)
+            const int xj = ne == 0 ? d.xoff[size_t(k)] : (ex[size_t(first)] & 0xffffff);
+            const int bo = ne == 0 ? zero_cf : eb[size_t(first)];
+            recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, xj * 16, bo * 16});
+            ext.insert(ext.end(), {0, mk, int(ents.size() / 2), std::max(ne - 1, 0)});
+            for (int e = 1; e < ne; ++e) {
+              ents.push_back(ex[size_t(first + e)]);
+              ents.push_back(eb[size_t(first + e)]);
+            }
+          } else {
+            // general step; split over mk lanes (backward, row r per lane:
+            // ext.x = 1 | 2 | r << 8), the coupling entries shared
+            recs.insert(recs.end(), {d.xoff[size_t(k)] * 16, pinv_off[size_t(st)] * 16, fwd ? -1 : 0, 0});
+            if (row <= 0) {
+              gen_first = int(ents.size() / 2);
+              for (int e = 0; e < ne; ++e) {
+                ents.push_back(ex[size_t(first + e)]);
+                ents.push_back(eb[size_t(first + e)]);
               }
             }
+            ext.insert(ext.end(), {row < 0 ? 1 : (3 | (row << 8)), mk, gen_first, ne});
+          }
+        };
+        for (int lv = 0; lv < nl; ++lv) {
+          const int c0 = off[size_t(lv)], cnt = off[size_t(lv) + 1] - c0;
+          for (int i = 0; i < cnt; ++nrounds) {
+            int used = 0;
+            while (i < cnt) {
+              const int st = steps[size_t(c0 + i)];
+              const int dm = demand(st);
+              if (used + dm > lanes) break;
+              for (int r = 0; r < dm; ++r) emit(st, dm > 1 ? r : -1);
+              used += dm;
+              ++i;
+            }
+            for (; used < lanes; ++used) empty();
+          }
         }
         for (int ln = 0; ln < lanes; ++ln) empty();  // padding round for the unconditional prefetch
       };

@@ -562,6 +562,34 @@ __device__ __forceinline__ void gen_bwd_step(const int4 rc, const int4 rx, unsig
   (void)x;
 }
 
+// One row r of a backward general step split over its m_k lanes: the row's
+// coupling sum acc_r (the loop of gen_bwd_step for that row alone), then,
+// after the lanes exchanged their sums, the row's pivot product.
+template <bool SM>
+__device__ __forceinline__ C2 gen_bwd_acc_row(const int4 rx, unsigned xs, unsigned cs, const double2* cf,
+                                              const int2* be, int r) {
+  const int mk = rx.y;
+  C2 acc = {0.0, 0.0};
+  for (int e = rx.z; e < rx.z + rx.w; ++e) {
+    const int2 en = be[e];
+    const int xj = en.x & 0xffffff, mj = en.x >> 24, bo = en.y;
+    C2 xv[3], Ar[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      xv[c] = lds2(xs + unsigned(xj + min(c, mj - 1)) * 16u);
+      Ar[c] = cfl<SM>(cs, cf, (bo + min(r, mk - 1) * mj + min(c, mj - 1)) * 16);
+    }
+    C2 u = {0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const C2 t = dev::cadd(u, dev::cmul(Ar[c], xv[c]));
+      u = c < mj ? t : u;
+    }
+    acc = dev::cadd(acc, u);
+  }
+  return acc;
+}
+
 // One forward elimination step of the lane-slot program (pull form): node k's
 // right-hand side minus its children's contributions in elimination order,
 // times pinv_k (solver.cpp:125-134; the scalar fast path and the general
@@ -741,8 +769,38 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
           if (e + q < e_end) acc = dev::cadd(acc, u[q]);
       }
       sts2(xs + rc.x, dev::csub(t, dev::cadd(C2{0.0, 0.0}, dev::cmul(pv, acc))));
-    } else if (rc.x >= 0) {
+    } else if (rc.x >= 0 && !(rx.x & 2)) {
       gen_bwd_step<SM>(rc, rx, xs, cs, x, cf, be);
+    }
+    // general steps split over their rows' lanes (host-assigned: ext.x bit 1,
+    // the row in bits 8..15): coupling sums per lane, exchanged by shuffle,
+    // then each lane's row of the pivot product
+    if (__any_sync(0xffffffffu, rc.x >= 0 && (rx.x & 2))) {
+      const bool sp = rc.x >= 0 && (rx.x & 2);
+      const int r = sp ? (rx.x >> 8) & 0xff : 0, mk = sp ? rx.y : 1, po = rc.y >> 4, xk = rc.x >> 4;
+      C2 Pr[3], xo = {0.0, 0.0}, accr = {0.0, 0.0};
+      if (sp) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Pr[c] = cfl<SM>(cs, cf, (po + r * mk + min(c, mk - 1)) * 16);
+        xo = lds2(xs + unsigned(xk + r) * 16u);
+        accr = gen_bwd_acc_row<SM>(rx, xs, cs, cf, be, r);
+      }
+      const int base = lane - r;
+      C2 ac[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int srcl = base + min(c, mk - 1);
+        ac[c] = C2{__shfl_sync(0xffffffffu, accr.x, srcl), __shfl_sync(0xffffffffu, accr.y, srcl)};
+      }
+      if (sp) {
+        C2 corr = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const C2 t = dev::cadd(corr, dev::cmul(Pr[c], ac[c]));
+          corr = c < mk ? t : corr;
+        }
+        sts2(xs + unsigned(xk + r) * 16u, dev::csub(xo, corr));
+      }
     }
     aa = aa_n;
     pv = pv_n;
