@@ -310,6 +310,14 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
   auto tab_s = [&](int b) { return reinterpret_cast<unsigned*>(base2 + b * buf_e); };
   auto bv_s = [&](int b) { return base2 + b * buf_e + lay.tab_e(); };
   auto z_s = [&](int b) { return base2 + b * buf_e + lay.tab_e() + lay.bv_e(); };
+  // the same slots as shared-space byte addresses for the copies (computed
+  // once: a generic -> shared conversion per copy re-reads the CTA's shared
+  // window register inside the tile loop)
+  unsigned sbase = unsigned(__cvta_generic_to_shared(smd));
+  asm volatile("mov.b32 %0, %0;" : "+r"(sbase));
+  auto tab_a = [&](int b) { return sbase + unsigned(b * buf_e) * 16u; };
+  auto bv_a = [&](int b) { return sbase + unsigned(b * buf_e + lay.tab_e()) * 16u; };
+  auto z_a = [&](int b) { return sbase + unsigned(b * buf_e + lay.tab_e() + lay.bv_e()) * 16u; };
   int* zcol = reinterpret_cast<int*>(base2 + 3 * lay.buf_e());  // [Gk][NL][2]
 
   const int4 cd = a.cand[c];
@@ -364,27 +372,27 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
   const unsigned long long zpol = S3_Z_EVICT_FIRST ? l2_evict_first_policy() : l2_evict_normal_policy();
   auto stage = [&](int j, int b) {
     const int t0 = j * K3;
-    for (int i = tid; i < K3 / 4; i += P) cp_async16(tab_s(b) + 4 * i, a.tab + t0 + 4 * i);
+    for (int i = tid; i < K3 / 4; i += P) cp_async16s(tab_a(b) + 16u * unsigned(i), a.tab + t0 + 4 * i);
     if (bv_fixed) {
       if (bv_in)
         for (int u = bv_u0; u < K3; u += bv_du) {
           const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-          cp_async16(bv_s(b) + size_t(u) * RS + bv_dst, a.bv + rho * 2 * L + bv_off);
+          cp_async16s(bv_a(b) + unsigned(u * RS + bv_dst) * 16u, a.bv + rho * 2 * L + bv_off);
         }
     } else {
       for (int i = tid; i < K3 * RS; i += P) {
         const int u = i / RS, ch = i - u * RS;
         if (ch % Ls >= nsc) continue;
         const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-        cp_async16(bv_s(b) + size_t(u) * RS + ch,
-                   a.bv + rho * 2 * L + size_t(ch / Ls) * L + size_t(sl) * Ls + size_t(ch % Ls));
+        cp_async16s(bv_a(b) + unsigned(u * RS + ch) * 16u,
+                    a.bv + rho * 2 * L + size_t(ch / Ls) * L + size_t(sl) * Ls + size_t(ch % Ls));
       }
     }
     for (int i = tid; i < nz; i += P) {
       const int u = i % K3;
       const int col = zcol[i / K3];
       const size_t rho = __ldg(a.tab + t0 + u) >> 3;
-      cp_async16_hint(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(col) * nphi + rho, zpol);
+      cp_async16s_hint(z_a(b) + unsigned(i + i / (NL * 2 * K3)) * 16u, a.Z + size_t(col) * nphi + rho, zpol);
     }
   };
   // Fast staging: each thread owns at most two bv rows and one table row of
@@ -410,20 +418,20 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
   };
   auto stage_fast = [&](int j, int b, const unsigned (&rr)[3]) {
     const int t0 = j * K3;
-    if (tid < K3 / 4) cp_async16(tab_s(b) + 4 * tid, a.tab + t0 + 4 * tid);
+    if (tid < K3 / 4) cp_async16s(tab_a(b) + 16u * unsigned(tid), a.tab + t0 + 4 * tid);
     if (bv_in) {
       if (u_a < K3)
-        cp_async16(bv_s(b) + size_t(u_a) * RS + bv_dst, a.bv + size_t(rr[0] >> 3) * 2 * L + bv_off);
+        cp_async16s(bv_a(b) + unsigned(u_a * RS + bv_dst) * 16u, a.bv + size_t(rr[0] >> 3) * 2 * L + bv_off);
       if (u_b < K3)
-        cp_async16(bv_s(b) + size_t(u_b) * RS + bv_dst, a.bv + size_t(rr[1] >> 3) * 2 * L + bv_off);
+        cp_async16s(bv_a(b) + unsigned(u_b * RS + bv_dst) * 16u, a.bv + size_t(rr[1] >> 3) * 2 * L + bv_off);
     }
     const size_t rz = rr[2] >> 3;
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (tid + q * P < nz) cp_async16_hint(z_s(b) + zdst[q], zsrc[q] + rz, zpol);
+      if (tid + q * P < nz) cp_async16s_hint(z_a(b) + unsigned(zdst[q]) * 16u, zsrc[q] + rz, zpol);
     // small CTAs (few scenarios): the remaining slots, same table row (P % K3 == 0)
     for (int i = tid + 4 * P; i < nz; i += P)
-      cp_async16_hint(z_s(b) + i + i / (NL * 2 * K3), a.Z + size_t(zcol[i / K3]) * nphi + rz, zpol);
+      cp_async16s_hint(z_a(b) + unsigned(i + i / (NL * 2 * K3)) * 16u, a.Z + size_t(zcol[i / K3]) * nphi + rz, zpol);
   };
   // D = Zs - Zr (scalar.cpp:16-17), once per (candidate, phase, row); each
   // thread's element offsets are fixed for the item (at most two per thread
