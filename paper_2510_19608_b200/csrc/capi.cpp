@@ -2,16 +2,20 @@
 // (include/kronred_b200.hpp): input parsing, problem construction and result
 // marshalling around the device Engine. Exceptions map to status codes the way
 // the reference CLI maps them to exit codes (main.cpp:234-246).
-#include <thread>
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
-#include <cmath>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <map>
+#include <mutex>
 #include <sstream>
+#include <thread>
 
 #include "kr_internal.hpp"
 
@@ -240,6 +244,84 @@ void zero_invalid(const Network& net, std::vector<double>& inj, int L) {
         }
 }
 
+// A small pool of host worker threads, created on first use and kept for the
+// process (a reload's per-scenario checks would otherwise pay a thread start
+// per worker on every call). parallel_for(n, fn) runs fn(0..n-1) and returns
+// when all are done; the caller works too. Concurrent callers (one host
+// thread per device) take turns.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  void parallel_for(size_t n, const std::function<void(size_t)>& fn) {
+    if (n == 0) return;
+    std::lock_guard<std::mutex> turn(call_m_);
+    if (workers_.empty() || n == 1) {
+      for (size_t i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    fn_ = &fn;
+    n_ = n;
+    next_ = 0;
+    busy_ = workers_.size();
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    run_tasks();
+    lk.lock();
+    done_cv_.wait(lk, [&] { return busy_ == 0; });
+    fn_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nw = std::min(15u, hw > 1 ? hw - 1 : 0u);
+    for (unsigned i = 0; i < nw; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  void run_tasks() {
+    for (;;) {
+      const size_t i = next_.fetch_add(1);
+      if (i >= n_) break;
+      (*fn_)(i);
+    }
+  }
+  void loop() {
+    unsigned long long seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(m_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      lk.unlock();
+      run_tasks();
+      lk.lock();
+      if (--busy_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_m_, m_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(size_t)>* fn_ = nullptr;
+  size_t n_ = 0;
+  std::atomic<size_t> next_{0};
+  size_t busy_ = 0;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+};
+
 // scenario_consistent (scenario.cpp:26-31): residual of Y V = I on non-slack
 // present-phase rows, relative to max(1, |I|_inf). Scenarios are independent:
 // they are checked on up to 16 host threads, and the first failing one (in
@@ -256,7 +338,8 @@ void check_residual(const Problem& p, const std::vector<double>& inj, const std:
   };
   std::vector<char> ok(L, 1);
   auto check = [&](size_t l0, size_t l1) {
-    std::vector<cx> yv(size_t(3 * n));
+    thread_local std::vector<cx> yv;
+    yv.resize(size_t(3 * n));
     for (size_t l = l0; l < l1; ++l) {
       const double* V = volt.data() + l * size_t(6 * n);
       const double* I = inj.data() + l * size_t(6 * n);
@@ -282,14 +365,10 @@ void check_residual(const Problem& p, const std::vector<double>& inj, const std:
       ok[l] = res <= 1e-10 * std::max(1.0, inorm) ? 1 : 0;
     }
   };
-  const size_t nt = std::min<size_t>(L, std::min<size_t>(16, std::max(1u, std::thread::hardware_concurrency())));
-  if (nt <= 1 || size_t(n) * L < 4096) {
+  if (size_t(n) * L < 4096)
     check(0, L);
-  } else {
-    std::vector<std::thread> th;
-    for (size_t t = 0; t < nt; ++t) th.emplace_back(check, L * t / nt, L * (t + 1) / nt);
-    for (auto& t : th) t.join();
-  }
+  else
+    HostPool::get().parallel_for(L, [&](size_t l) { check(l, l + 1); });
   for (size_t l = 0; l < L; ++l)
     if (!ok[l]) throw SolverError("scenario '" + ids[l] + "' failed the residual check");
 }

@@ -199,7 +199,20 @@ void validate_or_throw(const Network& net) {
     violation(os, bad, "slack-count", std::to_string(slack_count) + " slack nodes (need exactly 1)");
   if (slack_count == 1 && (slack < 0 || slack >= n || !(net.nodes[size_t(slack)].phases == PhaseMask::abc())))
     violation(os, bad, "slack-phases", "slack node must carry all three phases");
-  std::set<std::pair<int, int>> seen;
+  // duplicate endpoint pairs: every later branch of a pair reported, in branch order
+  std::vector<char> dup(net.branches.size(), 0);
+  {
+    std::vector<std::pair<std::pair<int, int>, size_t>> keys;
+    keys.reserve(net.branches.size());
+    for (size_t bi = 0; bi < net.branches.size(); ++bi) {
+      const Branch& b = net.branches[bi];
+      if (b.from < 0 || b.from >= n || b.to < 0 || b.to >= n || b.from == b.to) continue;
+      keys.push_back({std::minmax(b.from, b.to), bi});
+    }
+    std::sort(keys.begin(), keys.end());
+    for (size_t i = 1; i < keys.size(); ++i)
+      if (keys[i].first == keys[i - 1].first) dup[keys[i].second] = 1;
+  }
   for (size_t bi = 0; bi < net.branches.size(); ++bi) {
     const Branch& b = net.branches[bi];
     if (b.from < 0 || b.from >= n || b.to < 0 || b.to >= n) {
@@ -210,8 +223,7 @@ void validate_or_throw(const Network& net) {
       violation(os, bad, "self-loop", "branch #" + std::to_string(bi));
       continue;
     }
-    if (!seen.insert(std::minmax(b.from, b.to)).second)
-      violation(os, bad, "duplicate-branch", "branch #" + std::to_string(bi));
+    if (dup[bi]) violation(os, bad, "duplicate-branch", "branch #" + std::to_string(bi));
     const PhaseMask common = net.nodes[size_t(b.from)].phases.intersect(net.nodes[size_t(b.to)].phases);
     if (!b.y_series.confined_to(common))
       violation(os, bad, "branch-phase-leak", "branch #" + std::to_string(bi));
@@ -223,34 +235,54 @@ void validate_or_throw(const Network& net) {
   if (int(net.branches.size()) != n - 1)
     violation(os, bad, "not-radial", std::to_string(net.branches.size()) + " branches for " +
                                          std::to_string(n) + " nodes");
-  const auto adj = net.neighbor_lists();
+  // adjacency with branch ids (CSR; per node in branch order, as neighbor_lists)
+  std::vector<int> aoff(size_t(n) + 1, 0), adj_n, adj_b;
+  for (const Branch& b : net.branches)
+    if (b.from >= 0 && b.from < n && b.to >= 0 && b.to < n && b.from != b.to) {
+      ++aoff[size_t(b.from) + 1];
+      ++aoff[size_t(b.to) + 1];
+    }
+  for (int i = 0; i < n; ++i) aoff[size_t(i) + 1] += aoff[size_t(i)];
+  adj_n.resize(size_t(aoff[size_t(n)]));
+  adj_b.resize(adj_n.size());
+  {
+    std::vector<int> fill(aoff.begin(), aoff.end() - 1);
+    for (size_t bi = 0; bi < net.branches.size(); ++bi) {
+      const Branch& b = net.branches[bi];
+      if (b.from < 0 || b.from >= n || b.to < 0 || b.to >= n || b.from == b.to) continue;
+      adj_n[size_t(fill[size_t(b.from)])] = b.to;
+      adj_b[size_t(fill[size_t(b.from)]++)] = int(bi);
+      adj_n[size_t(fill[size_t(b.to)])] = b.from;
+      adj_b[size_t(fill[size_t(b.to)]++)] = int(bi);
+    }
+  }
   const int root = slack_count == 1 && slack >= 0 && slack < n ? slack : 0;
-  std::vector<int> parent(size_t(n), -2);
-  std::queue<int> q;
-  q.push(root);
+  std::vector<int> parent(size_t(n), -2), pbranch(size_t(n), -1);
+  std::vector<int> q;
+  q.reserve(size_t(n));
+  q.push_back(root);
   parent[size_t(root)] = -1;
-  int reached = 0;
-  while (!q.empty()) {
-    const int u = q.front();
-    q.pop();
-    ++reached;
-    for (int v : adj[size_t(u)])
+  for (size_t h = 0; h < q.size(); ++h) {
+    const int u = q[h];
+    for (int e = aoff[size_t(u)]; e < aoff[size_t(u) + 1]; ++e) {
+      const int v = adj_n[size_t(e)];
       if (parent[size_t(v)] == -2) {
         parent[size_t(v)] = u;
-        q.push(v);
+        pbranch[size_t(v)] = adj_b[size_t(e)];
+        q.push_back(v);
       }
+    }
   }
+  const int reached = int(q.size());
   if (reached != n) violation(os, bad, "disconnected", std::to_string(n - reached) + " nodes unreachable");
   if (slack_count == 1 && reached == n && int(net.branches.size()) == n - 1) {
-    std::map<std::pair<int, int>, const Branch*> bmap;
-    for (const Branch& b : net.branches) bmap[std::minmax(b.from, b.to)] = &b;
     for (int v = 0; v < n; ++v) {
       if (v == slack || parent[size_t(v)] < 0) continue;
       const PhaseMask child = net.nodes[size_t(v)].phases;
       const PhaseMask par = net.nodes[size_t(parent[size_t(v)])].phases;
       if (!child.subset_of(par))
         violation(os, bad, "phase-monotonicity", "node " + std::to_string(v) + " widens its parent's phases");
-      const Branch* b = bmap[std::minmax(v, parent[size_t(v)])];
+      const Branch* b = &net.branches[size_t(pbranch[size_t(v)])];
       for (int p = 0; p < 3 && b != nullptr; ++p) {
         if (!child.has(p)) continue;
         bool coupled = false;
@@ -616,6 +648,11 @@ FlatBlocks FlatBlocks::from(const BlockMatrix& y) {
   FlatBlocks f;
   f.n = y.n();
   f.row_off.assign(size_t(f.n) + 1, 0);
+  size_t nblk = 0;
+  for (int i = 0; i < f.n; ++i) nblk += y.row(i).size();
+  f.row.reserve(nblk);
+  f.col.reserve(nblk);
+  f.val.reserve(nblk * 18);
   for (int i = 0; i < f.n; ++i) {
     for (const auto& kv : y.row(i)) {
       f.row.push_back(i);
