@@ -34,11 +34,25 @@ struct S1Geom {
   static constexpr int BVR = kS1K * 16 / P;                  // bv rows per thread (16 chunks per row)
   static constexpr int ND = GK * kS1K;                       // D elements per tile
 };
-// dynamic shared memory of every score1 variant: 3 slots of the S = 1 ring
-// plus the column table
+// staging ring depth per split (tiles staged NS - 1 ahead): with S lanes per
+// pair a tile's compute is S times shorter, and at S = 2 a fourth slot hides
+// the copy latency (-0.8 us per mid-run iteration); S = 1 and S = 4 measure
+// best with three (tools/ring_ab.sh)
+#ifndef S1_NS1
+#define S1_NS1 3
+#endif
+#ifndef S1_NS2
+#define S1_NS2 4
+#endif
+#ifndef S1_NS4
+#define S1_NS4 3
+#endif
+template <int S>
+constexpr int s1_ns() { return S == 1 ? S1_NS1 : (S == 2 ? S1_NS2 : S1_NS4); }
+// dynamic shared memory of every score1 variant: the ring plus the column table
 template <int S, int GK>
 constexpr size_t s1_smem_bytes() {
-  return size_t(3) * S1Geom<S, GK>::BUF * sizeof(double2) + GK * 2 * sizeof(int) + 64;
+  return size_t(s1_ns<S>()) * S1Geom<S, GK>::BUF * sizeof(double2) + GK * 2 * sizeof(int) + 64;
 }
 
 // 4 plain rows at ring offsets u0..u0+3 (bvp: this pair's scenario column;
@@ -130,7 +144,8 @@ __device__ __forceinline__ void s1_item(const S3Args& a, int local, int g_count,
   const bool valid = cg < g_count && sl * kS1Ls + ll < L && myq == 0;
   const int c = min(cg, g_count - 1);  // the |phi(r)| = 1 group starts at candidate slot 0
   double2* base2 = reinterpret_cast<double2*>(smd);
-  int* zcol = reinterpret_cast<int*>(base2 + 3 * Geo::BUF);  // [GK][2]: Z columns of s and r
+  constexpr int NS = s1_ns<S>();
+  int* zcol = reinterpret_cast<int*>(base2 + NS * Geo::BUF);  // [GK][2]: Z columns of s and r
 
   const int4 cd = a.cand[c];
   const int s = cd.x, r = cd.y;
@@ -200,27 +215,28 @@ __device__ __forceinline__ void s1_item(const S3Args& a, int local, int g_count,
 
   double smice = 0.0, mx = 0.0, cm = 0.0;
   unsigned rn[Geo::BVR + 1];
-  load_rho(0, rn);
-  stage(0, 0, rn);
-  cp_async_commit();
-  load_rho(1, rn);
-  if (ntiles > 1) stage(1, 1, rn);
-  cp_async_commit();
-  load_rho(2, rn);
-  cp_async_wait1();
+  // prologue: tiles 0 .. NS - 2 in flight, then wait for tile 0
+#pragma unroll
+  for (int t = 0; t < NS - 1; ++t) {
+    load_rho(t, rn);
+    if (t < ntiles) stage(t, t, rn);
+    cp_async_commit();
+  }
+  load_rho(NS - 1, rn);
+  cp_async_wait_pending(NS - 2);
   __syncthreads();
   form_d(0);
   unsigned tflag_next = a.tplain[0];
   for (int j = 0; j < ntiles; ++j) {
-    const int b = j % 3;
+    const int b = j % NS;
     const bool tflag = tflag_next != 0u;
     if (j + 1 < ntiles) tflag_next = a.tplain[j + 1];
-    asm volatile("cp.async.wait_group 0;\n" ::);
+    cp_async_wait_pending(NS - 3);  // tile j + 1 has landed
     __syncthreads();
-    if (j + 2 < ntiles) stage(j + 2, (j + 2) % 3, rn);
+    if (j + NS - 1 < ntiles) stage(j + NS - 1, (j + NS - 1) % NS, rn);
     cp_async_commit();
-    load_rho(j + 3, rn);
-    if (j + 1 < ntiles) form_d((j + 1) % 3);
+    load_rho(j + NS, rn);
+    if (j + 1 < ntiles) form_d((j + 1) % NS);
     const double2* sb = slot(b);
     const unsigned* tb = reinterpret_cast<const unsigned*>(sb);
     const double2* bvp = sb + kS1TabE + ll + 4 * myq * 16;      // this lane's first pass
