@@ -288,7 +288,10 @@ struct Engine::Impl {
   }
   template <int S, int GK>
   void launch_s1_k(const S3Args& q, int grid, cudaStream_t st) {
-    score1_kernel<S, GK><<<grid, S1Geom<S, GK>::P, s1_smem_bytes<S, GK>(), st>>>(q);
+    constexpr size_t sm = s1_smem_bytes<S, GK>();
+    if (sm > 48 * 1024)  // (tuning geometries with a deep ring)
+      CK(cudaFuncSetAttribute(score1_kernel<S, GK>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    score1_kernel<S, GK><<<grid, S1Geom<S, GK>::P, sm, st>>>(q);
   }
   void launch_s1(int S, const S3Args& q, int grid, cudaStream_t st) {
     if (grid <= 0) return;
@@ -306,7 +309,10 @@ struct Engine::Impl {
   int s1_grid(int S, int items_max) {
     const int gk = s1_gk[s1_switch_index(S)];
     int occ = 0;
-    auto occ_of = [&](auto kern, int P, size_t sm) { CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P, sm)); };
+    auto occ_of = [&](auto kern, int P, size_t sm) {
+      if (sm > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P, sm));
+    };
     if (S == 1)
       gk == 16 ? occ_of(score1_kernel<1, 16>, 128, s1_smem_bytes<1, 16>()) : occ_of(score1_kernel<1, 8>, 64, s1_smem_bytes<1, 8>());
     else if (S == 2)
