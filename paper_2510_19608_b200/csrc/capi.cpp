@@ -404,11 +404,10 @@ void load_scenarios_from_host(Engine* eng, const Problem& p, const krg_host_prob
     inj.assign(hp.inj.begin(), hp.inj.end());
     zero_invalid(hp.net, inj, L);
     eng->set_scenarios(hp.ids, inj, {});
-    volt.resize(inj.size());
     const auto t0 = std::chrono::steady_clock::now();
-    eng->scenario_voltages(volt.data());
+    const std::vector<double>& vh = eng->vhat();
     const auto t1 = std::chrono::steady_clock::now();
-    check_residual(p, inj, volt, hp.ids);
+    check_residual(p, inj, vh, hp.ids);
     if (std::getenv("KRONRED_RELOAD_TRACE")) {
       auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
       std::fprintf(stderr, "scenarios: V-hat %.3f ms, residual %.3f ms\n", ms(t0, t1),
@@ -571,12 +570,13 @@ ScenarioLibrary load_library(const Network& net, const std::string& path) {
   auto eng = engine_from_host(hp, device_from_env());
   const int n = net.size();
   const Problem& p = eng->problem();
+  const std::vector<double>& vh = eng->vhat();
   for (size_t l = 0; l < hp.ids.size(); ++l) {
     Scenario sc;
     sc.id = hp.ids[l];
     for (int k = 0; k < 3 * n; ++k) {
       sc.injections.push_back(cx{p.injections[(l * 3 * n + size_t(k)) * 2], p.injections[(l * 3 * n + size_t(k)) * 2 + 1]});
-      sc.voltages.push_back(cx{p.voltages[(l * 3 * n + size_t(k)) * 2], p.voltages[(l * 3 * n + size_t(k)) * 2 + 1]});
+      sc.voltages.push_back(cx{vh[(l * 3 * n + size_t(k)) * 2], vh[(l * 3 * n + size_t(k)) * 2 + 1]});
     }
     lib.scenarios.push_back(std::move(sc));
   }

@@ -1256,7 +1256,6 @@ struct Engine::Impl {
     prob.L = L;
     prob.scenario_ids = ids;
     prob.injections = inj;
-    prob.voltages = volt;
     if (L == 0) return;
     d_inj.alloc(size_t(L) * 3 * n);
     h2d_staged(d_inj.p, inj.data(), inj.size() * sizeof(double));
@@ -1269,8 +1268,8 @@ struct Engine::Impl {
       solve_full(full, d_slackv.p, d_inj.p, L, d_vhat.p);
       h_vhat.resize(size_t(L) * 6 * n);
       d2h_staged(h_vhat.data(), d_vhat.p, h_vhat.size() * sizeof(double));
-      prob.voltages = h_vhat;
     }
+    prob.voltages.clear();  // (volt may alias it) V-hat lives in h_vhat (Engine::vhat)
     d_vhatp.alloc(size_t(nphi) * L);
     d_bv.alloc(size_t(nphi) * L * 2);
     d_iagg.alloc(size_t(n) * L * 3);
@@ -2233,6 +2232,8 @@ void Engine::set_exchange(int rank, int world, krg_exchange_fn fn, void* user) {
   impl_->xfn = fn;
   impl_->xuser = user;
 }
+
+const std::vector<double>& Engine::vhat() const { return impl_->h_vhat; }
 
 void Engine::scenario_voltages(double* out) {
   std::memcpy(out, impl_->h_vhat.data(), impl_->h_vhat.size() * sizeof(double));

@@ -137,6 +137,7 @@ class Engine {
 
   // scenario voltages (V-hat) [L][3n][2]
   void scenario_voltages(double* out);
+  const std::vector<double>& vhat() const;  // [L][3n][2] V-hat of the loaded library
   // batched anchored solve on the full Y
   void solve(const double* inj, int nrhs, double* out);
 
