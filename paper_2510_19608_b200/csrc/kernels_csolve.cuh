@@ -672,6 +672,11 @@ __device__ __forceinline__ void tree_forward(const BaseArgs& a, const int* M, un
   }
 }
 
+#ifndef BR_SUFFIX_UNROLL
+#define BR_SUFFIX_UNROLL 4
+#endif
+constexpr int kBrSuffixUnroll = BR_SUFFIX_UNROLL;  // rounds per iteration of the all-scalar suffix loop
+
 // Backward sweep of the lane-slot program (solver.cpp:136-147): every
 // eliminated node resolved against its (already final) couplings, one level
 // per round.
@@ -816,7 +821,7 @@ __device__ __forceinline__ void tree_backward(const BaseArgs& a, const int* M, u
   }
   // Suffix of all-scalar rounds (host-checked: every slot empty or a scalar
   // step with its single coupling): no vote, no extension records.
-#pragma unroll 2
+#pragma unroll (kBrSuffixUnroll)
   for (; br < nbr; ++br) {
 #ifdef BR_TRACE
     if (tr_on && br < 80) {
