@@ -217,8 +217,18 @@ struct Engine::Impl {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     // score1 (small networks): split once pairs x lanes fit one wave of 3
-    // resident CTAs per SM; score3 on large networks: about one CTA per SM
-    return s1_ok() ? (long long)sms * 3 * 128 : (long long)sms * 128;
+    // resident CTAs per SM; score3 on large networks: about one CTA per SM,
+    // with one or two scenarios 7/8 of one wave of the S = 2 launch (its CTAs
+    // stage half the Z slots, so more fit per SM; 8,381 / 5,991 nodes x 2
+    // scenarios: 8.9 -> 8.2 s / 4.5 -> 3.8 s, tools/s3fill_ab.sh)
+    if (s1_ok()) return (long long)sms * 3 * 128;
+    if (L <= 2) {
+      int oc = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, score3_kernel<0>, s3_threads(),
+                                                       S3Layout{s3_ls(), s3_slots(), 2}.smem_bytes()));
+      return std::max(1LL, (long long)sms * oc * s3_threads() * 7 / 8);
+    }
+    return (long long)sms * 128;
   }
   // slice-completion counters: one per candidate group at the widest split
   size_t s3_groups_max() const {
@@ -1953,6 +1963,14 @@ struct Engine::Impl {
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
       const int items_max = 4 * ((2 * nb + 4) / 5 + 3) * s3_nsl();  // up to 4 lanes per pair
       const int grid3 = std::max(1, std::min(items_max, std::max(1, occ) * sms));
+      size_t sm3s[3] = {sm3, sm3, sm3};
+      int grid3s[3] = {grid3, grid3, grid3};
+      for (int i = 1; i < 3 && !std::getenv("KRONRED_S3_FULL_SMEM"); ++i) {
+        sm3s[i] = S3Layout{s3_ls(), s3_slots(), i == 1 ? 2 : 4}.smem_bytes();
+        int oc = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, score3_kernel<0>, s3_threads(), sm3s[i]));
+        grid3s[i] = std::max(1, std::min(items_max, std::max(1, oc) * sms));
+      }
       const bool cplx = cfg.objective == Objective::complex_error;
       const bool s1 = s1_ok() && !cplx;  // (every created handle must drive a node)
       // one switch handle per unrolled copy (a handle drives one conditional
@@ -2031,8 +2049,8 @@ struct Engine::Impl {
         add_switch(stream, hsw[u], [&](int i, cudaStream_t cs) {
           if (i == 0)
             score3_kernel<1><<<grid3, s3_threads(), sm3, cs>>>(q);
-          else
-            score3_kernel<0><<<grid3, s3_threads(), sm3, cs>>>(q);
+          else  // S lanes per pair stage Z for G / S slots: a smaller CTA, a wider persistent grid
+            score3_kernel<0><<<grid3s[i], s3_threads(), sm3s[i], cs>>>(q);
           launched();
           CK(cudaGetLastError());
         });

@@ -69,15 +69,34 @@ struct S3Args {
   unsigned long long* tdbg;
 };
 
+// candidates per CTA for |phi(r)| = NL at S lanes per pair
+__host__ __device__ __forceinline__ int s3_cpc(int G, int NL, int S) { return G / NL / S > 1 ? G / NL / S : 1; }
+
 struct S3Layout {
   int Ls, G;
+  int S = 1;  // lanes per pair: a CTA stages Z for G / S slots (the host sizes each split's launch)
   __host__ __device__ size_t tab_e() const { return (K3 * 4 + 15) / 16; }  // double2 units
   __host__ __device__ size_t bv_e() const { return size_t(Ls) * K3 * 2; }
   // Zs and Zr staging; each candidate's block padded by one 16-byte slot so
-  // the candidates of a warp hit different banks
-  __host__ __device__ size_t z_e() const { return size_t(G) * (2 * K3 + 1); }
+  // the candidates of a warp hit different banks (the largest over |phi(r)|)
+  __host__ __device__ size_t z_e() const {
+    size_t m = 0;
+    for (int nl = 1; nl <= 3; ++nl) {
+      const size_t e = size_t(s3_cpc(G, nl, S)) * size_t(nl * 2 * K3 + 1);
+      m = e > m ? e : m;
+    }
+    return m;
+  }
+  __host__ __device__ size_t zcol_n() const {  // [Gk][NL][2] column indices
+    size_t m = 0;
+    for (int nl = 1; nl <= 3; ++nl) {
+      const size_t e = size_t(s3_cpc(G, nl, S)) * size_t(nl * 2);
+      m = e > m ? e : m;
+    }
+    return m;
+  }
   __host__ __device__ size_t buf_e() const { return tab_e() + bv_e() + z_e(); }
-  __host__ __device__ size_t smem_bytes() const { return 3 * buf_e() * sizeof(double2) + size_t(G) * 2 * sizeof(int) + 64; }
+  __host__ __device__ size_t smem_bytes() const { return 3 * buf_e() * sizeof(double2) + zcol_n() * sizeof(int) + 64; }
 };
 
 #ifndef S3_NNMAX
@@ -279,9 +298,6 @@ __device__ __forceinline__ void s3_handoff(double& smice, double& cm, int q, int
   cm = __shfl_sync(0xffffffffu, cm, src);
 }
 
-// candidates per CTA of the |phi(r)| = NL group at S lanes per pair
-__host__ __device__ __forceinline__ int s3_cpc(int G, int NL, int S) { return G / NL / S > 1 ? G / NL / S : 1; }
-
 // One work item (a group of candidates x one scenario slice). SF = 1: the
 // one-lane-per-pair program compiled on its own (S = 1); SF = 0: S lanes per
 // pair from the argument.
@@ -301,7 +317,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
   const int cg = cgrp * Gk + gl;
   const bool valid = pr < Gk * Ls && cg < g_count && sl * Ls + ll < L && myq == 0;
   const int c = g_begin + min(cg, g_count - 1);
-  const S3Layout lay{Ls, a.G};
+  const S3Layout lay{Ls, a.G, S};
   double2* base2 = reinterpret_cast<double2*>(smd);
   // staging ring: 3 slots sized for this item's candidates (a deeper ring
   // measured no faster: the copy latency is covered by one tile's compute)
