@@ -225,7 +225,7 @@ struct Engine::Impl {
     if (L <= 2) {
       int oc = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, score3_kernel<0>, s3_threads(),
-                                                       S3Layout{s3_ls(), s3_slots(), 2}.smem_bytes()));
+                                                       S3Layout{s3_ls(), s3_slots(), 2, S3_NS_SPLIT}.smem_bytes()));
       return std::max(1LL, (long long)sms * oc * s3_threads() * 7 / 8);
     }
     return (long long)sms * 128;
@@ -1966,7 +1966,7 @@ struct Engine::Impl {
       size_t sm3s[3] = {sm3, sm3, sm3};
       int grid3s[3] = {grid3, grid3, grid3};
       for (int i = 1; i < 3 && !std::getenv("KRONRED_S3_FULL_SMEM"); ++i) {
-        sm3s[i] = S3Layout{s3_ls(), s3_slots(), i == 1 ? 2 : 4}.smem_bytes();
+        sm3s[i] = S3Layout{s3_ls(), s3_slots(), i == 1 ? 2 : 4, S3_NS_SPLIT}.smem_bytes();
         int oc = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, score3_kernel<0>, s3_threads(), sm3s[i]));
         grid3s[i] = std::max(1, std::min(items_max, std::max(1, oc) * sms));

@@ -72,9 +72,18 @@ struct S3Args {
 // candidates per CTA for |phi(r)| = NL at S lanes per pair
 __host__ __device__ __forceinline__ int s3_cpc(int G, int NL, int S) { return G / NL / S > 1 ? G / NL / S : 1; }
 
+// The row-split program (SF = 0, S = 2 or 4) runs a two-slot ring instead: it
+// waits for tile j + 1 and forms its D after computing tile j (two barriers per
+// tile) in 2/3 of the shared memory (5,991 nodes x 2 scenarios: -2 %,
+// tools/s3ns_ab.sh; S3_NS_SPLIT=3 gives it the three-slot ring).
+#ifndef S3_NS_SPLIT
+#define S3_NS_SPLIT 2
+#endif
+
 struct S3Layout {
   int Ls, G;
-  int S = 1;  // lanes per pair: a CTA stages Z for G / S slots (the host sizes each split's launch)
+  int S = 1;
+  int NS = 3;  // ring slots  // lanes per pair: a CTA stages Z for G / S slots (the host sizes each split's launch)
   __host__ __device__ size_t tab_e() const { return (K3 * 4 + 15) / 16; }  // double2 units
   __host__ __device__ size_t bv_e() const { return size_t(Ls) * K3 * 2; }
   // Zs and Zr staging; each candidate's block padded by one 16-byte slot so
@@ -96,7 +105,7 @@ struct S3Layout {
     return m;
   }
   __host__ __device__ size_t buf_e() const { return tab_e() + bv_e() + z_e(); }
-  __host__ __device__ size_t smem_bytes() const { return 3 * buf_e() * sizeof(double2) + zcol_n() * sizeof(int) + 64; }
+  __host__ __device__ size_t smem_bytes() const { return size_t(NS) * buf_e() * sizeof(double2) + zcol_n() * sizeof(int) + 64; }
 };
 
 #ifndef S3_NNMAX
@@ -319,10 +328,10 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
   const int c = g_begin + min(cg, g_count - 1);
   const S3Layout lay{Ls, a.G, S};
   double2* base2 = reinterpret_cast<double2*>(smd);
-  // staging ring: 3 slots sized for this item's candidates (a deeper ring
+  // staging ring: NS slots sized for this item's candidates (a deeper ring
   // measured no faster: the copy latency is covered by one tile's compute)
   const size_t buf_e = lay.tab_e() + lay.bv_e() + size_t(Gk) * (NL * 2 * K3 + 1);
-  constexpr int NS = 3;
+  constexpr int NS = SF ? 3 : S3_NS_SPLIT;
   auto tab_s = [&](int b) { return reinterpret_cast<unsigned*>(base2 + b * buf_e); };
   auto bv_s = [&](int b) { return base2 + b * buf_e + lay.tab_e(); };
   auto z_s = [&](int b) { return base2 + b * buf_e + lay.tab_e() + lay.bv_e(); };
@@ -334,7 +343,7 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
   auto tab_a = [&](int b) { return sbase + unsigned(b * buf_e) * 16u; };
   auto bv_a = [&](int b) { return sbase + unsigned(b * buf_e + lay.tab_e()) * 16u; };
   auto z_a = [&](int b) { return sbase + unsigned(b * buf_e + lay.tab_e() + lay.bv_e()) * 16u; };
-  int* zcol = reinterpret_cast<int*>(base2 + 3 * lay.buf_e());  // [Gk][NL][2]
+  int* zcol = reinterpret_cast<int*>(base2 + NS * lay.buf_e());  // [Gk][NL][2]
 
   const int4 cd = a.cand[c];
   const int s = cd.x, r = cd.y;
@@ -481,23 +490,33 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
 #ifdef S3_TIMING  // tuning aid: per-phase cycle counts of CTA 0's warps
   long long tm_pro = clock64(), tm_wait = 0, tm_stage = 0, tm_rho = 0, tm_fd = 0, tm_comp = 0, tm_x;
 #endif
-  // prologue: tiles 0 and 1 in flight, then wait for tile 0
+  // prologue: tiles 0 and 1 in flight (two slots: tile 0), then wait for tile 0
   if (fst) {
     unsigned r0[3], r1[3];
     load_rho(0, r0);
     load_rho(1, r1);
     stage_fast(0, 0, r0);
     cp_async_commit();
-    if (ntiles > 1) stage_fast(1, 1, r1);
-    cp_async_commit();
-    load_rho(2, rn);
+    if (NS == 3) {
+      if (ntiles > 1) stage_fast(1, 1, r1);
+      cp_async_commit();
+      load_rho(2, rn);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) rn[q] = r1[q];
+    }
   } else {
     stage(0, 0);
     cp_async_commit();
-    if (ntiles > 1) stage(1, 1);
-    cp_async_commit();
+    if (NS == 3) {
+      if (ntiles > 1) stage(1, 1);
+      cp_async_commit();
+    }
   }
-  cp_async_wait1();
+  if (NS == 3)
+    cp_async_wait1();
+  else
+    asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   form_d(0);
 #ifdef S3_TIMING
@@ -505,39 +524,40 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
 #endif
   unsigned tflag_next = a.tplain[0];  // raw byte: tested one tile later
   for (int j = 0; j < ntiles; ++j) {
-    const int b = j % 3;
+    const int b = j % NS;
     const bool tflag = tflag_next != 0u;
     if (j + 1 < ntiles) tflag_next = a.tplain[j + 1];
 #ifdef S3_TIMING
     tm_x = clock64();
 #endif
-    asm volatile("cp.async.wait_group 0;\n" ::);  // tile j + 1 has landed
-    __syncthreads();
+    if (NS == 3) asm volatile("cp.async.wait_group 0;\n" ::);  // tile j + 1 has landed
+    __syncthreads();  // (two slots: tile j's D is formed, tile j - 1's slot is free)
 #ifdef S3_TIMING
     tm_wait += clock64() - tm_x;
     tm_x = clock64();
 #endif
+    const int jn = j + NS - 1;  // the tile staged now
     if (fst) {
-      if (j + 2 < ntiles) stage_fast(j + 2, (j + 2) % 3, rn);
+      if (jn < ntiles) stage_fast(jn, jn % NS, rn);
       cp_async_commit();
 #ifdef S3_TIMING
       tm_stage += clock64() - tm_x;
       tm_x = clock64();
 #endif
-      load_rho(j + 3, rn);  // consumed next iteration: latency hidden by this tile's compute
+      load_rho(jn + 1, rn);  // consumed next iteration: latency hidden by this tile's compute
 #ifdef S3_TIMING
       tm_rho += clock64() - tm_x;
       tm_x = clock64();
 #endif
     } else {
-      if (j + 2 < ntiles) stage(j + 2, (j + 2) % 3);
+      if (jn < ntiles) stage(jn, jn % NS);
       cp_async_commit();
     }
 #ifdef S3_TIMING
     tm_stage += clock64() - tm_x;
     tm_x = clock64();
 #endif
-    if (j + 1 < ntiles) form_d((j + 1) % 3);
+    if (NS == 3 && j + 1 < ntiles) form_d((j + 1) % 3);
 #ifdef S3_TIMING
     tm_fd += clock64() - tm_x;
     tm_x = clock64();
@@ -594,6 +614,11 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
 #ifdef S3_TIMING
     tm_comp += clock64() - tm_x;
 #endif
+    if (NS == 2 && j + 1 < ntiles) {  // two slots: tile j + 1 lands, then its D
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      __syncthreads();
+      form_d((j + 1) & 1);
+    }
   }
   smice = dev::dadd(smice, cm);
   for (int o = 1; o < S; o <<= 1) mx = s3max(mx, __shfl_xor_sync(0xffffffffu, mx, o));  // order-free
