@@ -1581,8 +1581,8 @@ struct Engine::Impl {
       } else if (c3 > 0) {
         if (q.S == 1)
           score3_kernel<1><<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
-        else
-          score3_kernel<0><<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots()}.smem_bytes(), stream>>>(q);
+        else  // the split program stages G / S slots in its own ring
+          score3_kernel<0><<<c3, s3_threads(), S3Layout{s3_ls(), s3_slots(), q.S, S3_NS_SPLIT}.smem_bytes(), stream>>>(q);
         launched();
         CK(cudaGetLastError());
       }
