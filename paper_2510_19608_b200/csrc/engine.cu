@@ -230,6 +230,13 @@ struct Engine::Impl {
     }
     return (long long)sms * 128;
   }
+  // S = 4 starts at this many sixteenths of the fill: with one or two scenarios
+  // on a large network at 14 (S = 4 wins below ~3/4 of its own wave: C4 / C3
+  // L = 2 per-bucket sweep, tools/s3fill4_ab.sh), otherwise S3_FILL4_16
+  int s3_fill4_16() const {
+    if (const char* e = std::getenv("KRONRED_S3_FILL4")) return std::atoi(e);
+    return !s1_ok() && L <= 2 ? 14 : S3_FILL4_16;
+  }
   // slice-completion counters: one per candidate group at the widest split
   size_t s3_groups_max() const {
     size_t g = 8;
@@ -1540,7 +1547,7 @@ struct Engine::Impl {
       S3Args q = s3_args();
       q.C = int(C);
       q.R = R;
-      q.S = s3_lanes(C * L, s3_fill(), s3_force);
+      q.S = s3_lanes(C * L, s3_fill(), s3_force, s3_fill4_16());
       int c3 = 0;
       for (int k = 1; k <= 3; ++k) {
         const int cpc = !s1_ok() ? s3_cpc(s3_slots(), k, q.S)
@@ -1752,6 +1759,7 @@ struct Engine::Impl {
     for (int i = 0; i < 3; ++i) a.gk1[i] = s1_ok() ? s1_gk[i] : 0;
     a.s_multi = s3_multi_lanes();
     a.fill = s3_fill();
+    a.fill4_16 = s3_fill4_16();
     a.force_s = s3_force;
     a.ldc = s3_ldc();  // max_err is scenario-major; per-candidate SMICE in pcand
     a.complex_obj = cfg.objective == Objective::complex_error ? 1 : 0;
@@ -1981,7 +1989,7 @@ struct Engine::Impl {
         // property of the network (the graph is keyed on it)
         std::vector<int> c0s, c0r;
         hs.enumerate(c0s, c0r);
-        const int S0 = s3_lanes((long long)c0s.size() * L, s3_fill(), s3_force);
+        const int S0 = s3_lanes((long long)c0s.size() * L, s3_fill(), s3_force, s3_fill4_16());
         for (int u = 0; u < kLoopUnroll; ++u)
           CK(cudaGraphConditionalHandleCreate(&hsw[u], body, unsigned(u == 0 ? s1_switch_index(S0) : 0),
                                               cudaGraphCondAssignDefault));

@@ -34,6 +34,7 @@ struct LoopArgs {
   int gk1[3];          // score1 candidates per CTA at S = 1, 2, 4 (0: score3 takes |phi(r)| = 1 too)
   int s_multi;         // score3's split for the |phi(r)| >= 2 groups when score1 runs
   long long fill;      // scorer row split: thread budget (s3_lanes)
+  int fill4_16;        // S = 4 threshold in sixteenths of the budget
   int force_s;         // scorer row split forced to 1/2/4 (0: automatic)
   int inc_enum;        // 1: incremental candidate list after a commit (else full rebuild)
   int kcap;            // keys region size (power of two >= 2 nb); the previous list follows it
@@ -535,7 +536,7 @@ __global__ void __launch_bounds__(kLoopThreads) enum_kernel(LoopArgs a) {
   }
   if (tid == 0) {
     const int cnt3 = Cl - cnt1 - cnt2;
-    const int S = s3_lanes((long long)Cl * a.L, a.fill, a.force_s);
+    const int S = s3_lanes((long long)Cl * a.L, a.fill, a.force_s, a.fill4_16);
     const int gk1 = a.gk1[S == 1 ? 0 : (S == 2 ? 1 : 2)];
     const int Sm = gk1 > 0 ? a.s_multi : S;  // split of the |phi(r)| >= 2 groups
     const int cpc1 = gk1 > 0 ? gk1 : s3_cpc(a.G3, 1, S), cpc2 = s3_cpc(a.G3, 2, Sm), cpc3 = s3_cpc(a.G3, 3, Sm);

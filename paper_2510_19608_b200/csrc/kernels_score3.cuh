@@ -683,9 +683,9 @@ __device__ __forceinline__ void s3_body(const S3Args& a, int S_arg, int local, i
 #ifndef S3_FILL4_16  // the S = 4 threshold as a fraction of the budget, in sixteenths
 #define S3_FILL4_16 11
 #endif
-__host__ __device__ __forceinline__ int s3_lanes(long long pairs, long long fill, int force) {
+__host__ __device__ __forceinline__ int s3_lanes(long long pairs, long long fill, int force, int fill4_16 = S3_FILL4_16) {
   if (force == 1 || force == 2 || force == 4) return force;
-  if (pairs * 4 * 16 <= fill * S3_FILL4_16) return 4;
+  if (pairs * 4 * 16 <= fill * fill4_16) return 4;
   if (pairs * 2 * 16 <= fill * S3_FILL2_16) return 2;
   return 1;
 }
